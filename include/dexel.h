@@ -1,0 +1,135 @@
+/* dexel.h -- C ABI of the B200 dexel offset library (libdexel.so).
+ *
+ * Hot path of arXiv 1804.08968 "Half-Space Power Diagrams and Discrete
+ * Surface Offsets": the separable two-pass dilation / erosion of a 3D dexel
+ * buffer, plus the shell D \ E.
+ *
+ * Data model ("a set of parallel segments arranged in a 2D
+ * grid, where each cell S_ij ... contains a list of segments"): an nx x ny
+ * grid of columns; column c = j*nx + i (i fastest) holds a canonical list of
+ * CLOSED intervals [z_in, z_out] along z, strictly increasing
+ * (z_in_0 < z_out_0 < z_in_1 < ...), fp32, in a LOCAL frame z - z_ref chosen
+ * by the caller (reading R9), all inside the domain [z_lo, z_hi].
+ * The domain U = grid footprint x [z_lo, z_hi] is also the complement domain
+ * (neutral boundary, reading R6): out-of-grid columns are absent,
+ * dilations are clipped to U, erosion is U \ D_r(U \ S).
+ *
+ * Every call returns dexel_status (0 = OK); nothing throws across the ABI.
+ * On error, dexel_last_error() (thread-local) describes the failure.
+ * One handle = one grid (or one y-slab of it) on one device and one stream;
+ * handles are not re-entrant.  All device work is stream-ordered on the
+ * handle's stream; calls that return sizes to the host synchronise it.
+ */
+#ifndef DEXEL_H
+#define DEXEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dexel_grid_s* dexel_grid;
+
+typedef enum {
+  DEXEL_OK = 0,
+  DEXEL_EINVAL = 1,     /* invalid argument or invalid input data */
+  DEXEL_ENOMEM = 2,     /* device allocation failed */
+  DEXEL_EMISMATCH = 3,  /* src/dst geometry differs */
+  DEXEL_EOVERFLOW = 4,  /* caller buffer too small (see dexel_size) or a column exceeds a kernel limit */
+  DEXEL_ECUDA = 5,      /* CUDA runtime error */
+  DEXEL_ENCCL = 6       /* NCCL error (multi-GPU) */
+} dexel_status;
+
+typedef struct {
+  int32_t nx, ny;       /* global grid columns, >= 1 */
+  double spacing;       /* lateral dexel spacing s > 0 (1.0 in all configs) */
+  double z_ref;         /* world z of local value 0 (informational; all data are local) */
+  float z_lo, z_hi;     /* domain in the local frame, finite, z_lo < z_hi */
+  int32_t device;       /* CUDA ordinal */
+  void* stream;         /* cudaStream_t; NULL -> library-owned stream */
+  void* nccl_comm;      /* ncclComm_t or NULL (single GPU / caller-managed halos) */
+  int32_t rank, nranks; /* slab owner; 0,1 for a single GPU */
+  int32_t y0, y1;       /* owned global rows [y0,y1); 0,ny for a single GPU */
+} dexel_desc;
+
+/* Create an empty grid (all columns empty).  *out receives the handle. */
+dexel_status dexel_create(const dexel_desc* d, dexel_grid* out);
+
+/* Replace the grid contents with a canonical CSR of the handle's local rows.
+ *   offsets:   uint64[ncols_local + 1], offsets[0] = 0, non-decreasing,
+ *              offsets[ncols_local] = n_intervals  (ncols_local = nx*(y1-y0))
+ *   endpoints: float[2*n_intervals], (z_in, z_out) pairs, local frame
+ *   src_on_device: 0 -> host pointers (pageable or pinned), 1 -> device pointers
+ *              (read only during the call, stream-ordered).
+ * Validation (on the device): per column strictly increasing, finite, inside
+ * [z_lo, z_hi]; offsets monotone.  Failure -> DEXEL_EINVAL, last_error names
+ * the first bad column, the grid is left unchanged.  Synchronises the stream. */
+dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* endpoints,
+                          uint64_t n_intervals, int src_on_device);
+
+/* dst := D_r(src): Eq. 1 on the ray lattice, computed by
+ * the two passes (pass 1 along x: closest-parent extrusion P:494-501; pass 2
+ * along y: power dilation with weights r^2 - d^2), clipped to U.
+ * r finite, >= 0; R = floor(r/spacing) <= 255.  src and dst must share the
+ * geometry (EMISMATCH) and differ (EINVAL).  dst is replaced; on error it is
+ * left empty.  Output is canonical and bitwise deterministic.  Synchronises
+ * the stream up to three times (allocation sizes). */
+dexel_status dexel_dilate(dexel_grid src, float r, dexel_grid dst);
+
+/* dst := E_r(src) = U \ D_r(U \ src).  Same rules. */
+dexel_status dexel_erode(dexel_grid src, float r, dexel_grid dst);
+
+/* dst := D_rout(src) \ E_rin(src) = D_rout(src) n D_rin(U \ src), per column
+ * (the thick shell of PAPER.md:58-61, :847-849).  Same rules. */
+dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst);
+
+/* Number of intervals currently held (local slab). */
+dexel_status dexel_size(dexel_grid g, uint64_t* n_intervals);
+
+/* Copy the grid out as CSR (offsets: ncols_local+1 entries; endpoints:
+ * 2*n floats).  capacity_intervals < n -> DEXEL_EOVERFLOW (nothing written).
+ * dst_on_device: 0 host, 1 device pointers.  Synchronises the stream. */
+dexel_status dexel_download(dexel_grid g, uint64_t* offsets, float* endpoints,
+                            uint64_t capacity_intervals, int dst_on_device);
+
+/* Pass 1 alone (the intermediate S_Mid of PAPER.md:494-501), exposed for
+ * parity testing: for every column of src (or of U \ src when complement=1)
+ * the closest-parent extrusion along x as maximal closed pieces
+ * (lo, hi, kappa), kappa = min |dx| over parents within R = floor(r/s).
+ *   offsets: uint64[ncols_local+1]; z: float[2*m]; kappa: uint8[m]
+ * *n_pieces always receives m; capacity < m -> DEXEL_EOVERFLOW. */
+dexel_status dexel_pass1(dexel_grid src, float r, int complement, uint64_t* offsets, float* z,
+                         uint8_t* kappa, uint64_t capacity_pieces, uint64_t* n_pieces,
+                         int dst_on_device);
+
+/* Wait for all work queued on the handle's stream. */
+dexel_status dexel_sync(dexel_grid g);
+
+/* Destroy a handle and free its device memory (NULL-safe). */
+void dexel_destroy(dexel_grid g);
+
+/* Thread-local description of the last error ("" if none). */
+const char* dexel_last_error(void);
+
+/* Route device allocations through a caller allocator (e.g. the PyTorch
+ * caching allocator).  NULL,NULL restores cudaMallocAsync/cudaFreeAsync.
+ * Must be called while no handle holds memory. */
+typedef void* (*dexel_alloc_fn)(size_t bytes, int device, void* stream, void* ctx);
+typedef void (*dexel_free_fn)(void* ptr, size_t bytes, int device, void* stream, void* ctx);
+dexel_status dexel_set_allocator(dexel_alloc_fn alloc, dexel_free_fn free_, void* ctx);
+
+/* Per-op statistics of the last op on handle g (for measurement):
+ * n_in, n_mid (pass-1 pieces), n_lev (level intervals), n_out, and device
+ * time of each stage in ms (0 if not timed).  stage_ms needs 4 entries. */
+typedef struct {
+  uint64_t n_in, n_mid, n_lev, n_out;
+  float stage_ms[4];
+} dexel_stats;
+dexel_status dexel_last_stats(dexel_grid g, dexel_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEXEL_H */

@@ -1,0 +1,238 @@
+"""B200-native separable dexel offsets (arXiv 1804.08968) -- Python binding.
+
+Thin ctypes marshalling over libdexel.so (the C ABI declared in
+include/dexel.h).  Every step of the path runs in the library's CUDA
+kernels; this module only moves pointers, sizes and status codes.  There is
+no CPU fallback: if the shared library is missing, every call raises.
+
+PyTorch is used only for device memory (optional caching-allocator hook),
+streams and -- in multi-process code -- process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdexel.so")
+
+DEXEL_OK, DEXEL_EINVAL, DEXEL_ENOMEM, DEXEL_EMISMATCH, DEXEL_EOVERFLOW, DEXEL_ECUDA, DEXEL_ENCCL = range(7)
+_STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA", 6: "ENCCL"}
+
+# every symbol include/dexel.h declares (checked by tests/test_abi.py)
+EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_size",
+           "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
+           "dexel_set_allocator", "dexel_last_stats"]
+
+
+class DexelError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"dexel {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class dexel_desc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("spacing", ctypes.c_double),
+                ("z_ref", ctypes.c_double), ("z_lo", ctypes.c_float), ("z_hi", ctypes.c_float),
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("y0", ctypes.c_int32),
+                ("y1", ctypes.c_int32)]
+
+
+class dexel_stats(ctypes.Structure):
+    _fields_ = [("n_in", ctypes.c_uint64), ("n_mid", ctypes.c_uint64), ("n_lev", ctypes.c_uint64),
+                ("n_out", ctypes.c_uint64), ("stage_ms", ctypes.c_float * 4)]
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+
+_lib = None
+
+
+def lib():
+    """Load libdexel.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u64, u64p = ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)
+        sig = {
+            "dexel_create": ([ctypes.POINTER(dexel_desc), ctypes.POINTER(vp)], ctypes.c_int),
+            "dexel_upload": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
+            "dexel_dilate": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_erode": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_shell": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_size": ([vp, u64p], ctypes.c_int),
+            "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
+            "dexel_pass1": ([vp, ctypes.c_float, ctypes.c_int, vp, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
+            "dexel_sync": ([vp], ctypes.c_int),
+            "dexel_destroy": ([vp], None),
+            "dexel_last_error": ([], ctypes.c_char_p),
+            "dexel_set_allocator": ([ALLOC_FN, FREE_FN, vp], ctypes.c_int),
+            "dexel_last_stats": ([vp, ctypes.POINTER(dexel_stats)], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != DEXEL_OK:
+        raise DexelError(status, lib().dexel_last_error().decode())
+
+
+def _ptr(a) -> int:
+    """data pointer of a numpy array or torch tensor"""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _is_dev(a) -> bool:
+    return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+# ---------------------------------------------------------------- allocator hook
+_alloc_refs = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route library device allocations through the PyTorch caching allocator."""
+    global _alloc_refs
+    L = lib()
+    if not enable:
+        _check(L.dexel_set_allocator(ALLOC_FN(), FREE_FN(), None))
+        _alloc_refs = None
+        return
+    import torch
+
+    def _alloc(nbytes, device, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), int(device), stream)
+        except Exception:  # noqa: BLE001 -- reported to C as NULL -> DEXEL_ENOMEM
+            return None
+
+    def _free(ptr, nbytes, device, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    _alloc_refs = (ALLOC_FN(_alloc), FREE_FN(_free))
+    _check(L.dexel_set_allocator(_alloc_refs[0], _alloc_refs[1], None))
+
+
+# ---------------------------------------------------------------- grid handle
+class Grid:
+    """A dexel buffer on one device (one handle of the C ABI)."""
+
+    def __init__(self, nx: int, ny: int, z_lo: float, z_hi: float, z_ref: float = 0.0, spacing: float = 1.0,
+                 device: int = 0, stream: Optional[int] = None, y0: int = 0, y1: Optional[int] = None,
+                 rank: int = 0, nranks: int = 1, nccl_comm: Optional[int] = None):
+        self.desc = dexel_desc(nx, ny, spacing, z_ref, z_lo, z_hi, device, stream, nccl_comm, rank, nranks,
+                               y0, ny if y1 is None else y1)
+        h = ctypes.c_void_p()
+        _check(lib().dexel_create(ctypes.byref(self.desc), ctypes.byref(h)))
+        self.h = h
+
+    @classmethod
+    def like(cls, g: "Grid") -> "Grid":
+        d = g.desc
+        return cls(d.nx, d.ny, d.z_lo, d.z_hi, d.z_ref, d.spacing, d.device, d.stream, d.y0, d.y1, d.rank,
+                   d.nranks, d.nccl_comm)
+
+    @classmethod
+    def from_host(cls, hg, device: int = 0, stream: Optional[int] = None) -> "Grid":
+        """from a dexelgen.Grid-like object (nx, ny, off, ep, z_lo, z_hi, z_ref, spacing)"""
+        g = cls(hg.nx, hg.ny, hg.z_lo, hg.z_hi, getattr(hg, "z_ref", 0.0), getattr(hg, "spacing", 1.0), device,
+                stream)
+        g.upload(hg.off, hg.ep)
+        return g
+
+    @property
+    def ncol(self) -> int:
+        return self.desc.nx * (self.desc.y1 - self.desc.y0)
+
+    def upload(self, off, ep):
+        if isinstance(off, np.ndarray):
+            off = np.ascontiguousarray(off, dtype=np.uint64)
+            ep = np.ascontiguousarray(ep, dtype=np.float32)
+        n = (int(off[-1]) if isinstance(off, np.ndarray) else int(ep.numel()) // 2)
+        _check(lib().dexel_upload(self.h, _ptr(off), _ptr(ep) if n else None, n, 1 if _is_dev(off) else 0))
+
+    def size(self) -> int:
+        n = ctypes.c_uint64()
+        _check(lib().dexel_size(self.h, ctypes.byref(n)))
+        return n.value
+
+    def download(self, device: bool = False):
+        n = self.size()
+        if device:
+            import torch
+            dev = torch.device("cuda", self.desc.device)
+            off = torch.empty(self.ncol + 1, dtype=torch.int64, device=dev)
+            ep = torch.empty(max(2 * n, 2), dtype=torch.float32, device=dev)
+            _check(lib().dexel_download(self.h, off.data_ptr(), ep.data_ptr(), n, 1))
+            return off, ep[:2 * n]
+        off = np.empty(self.ncol + 1, dtype=np.uint64)
+        ep = np.empty(max(2 * n, 2), dtype=np.float32)
+        _check(lib().dexel_download(self.h, off.ctypes.data, ep.ctypes.data, n, 0))
+        return off, ep[:2 * n]
+
+    def stats(self) -> dict:
+        s = dexel_stats()
+        _check(lib().dexel_last_stats(self.h, ctypes.byref(s)))
+        return dict(n_in=s.n_in, n_mid=s.n_mid, n_lev=s.n_lev, n_out=s.n_out, stage_ms=list(s.stage_ms))
+
+    def sync(self):
+        _check(lib().dexel_sync(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().dexel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+# ---------------------------------------------------------------- operations (same names as the C ABI)
+def dexel_dilate(src: Grid, r: float, dst: Grid) -> Grid:
+    _check(lib().dexel_dilate(src.h, float(r), dst.h))
+    return dst
+
+
+def dexel_erode(src: Grid, r: float, dst: Grid) -> Grid:
+    _check(lib().dexel_erode(src.h, float(r), dst.h))
+    return dst
+
+
+def dexel_shell(src: Grid, r_out: float, r_in: float, dst: Grid) -> Grid:
+    _check(lib().dexel_shell(src.h, float(r_out), float(r_in), dst.h))
+    return dst
+
+
+def dexel_pass1(src: Grid, r: float, complement: bool = False):
+    """S_Mid pieces of pass 1 -> (offsets uint64[ncol+1], z float32[2m], kappa uint8[m]) on the host."""
+    L = lib()
+    m = ctypes.c_uint64()
+    st = L.dexel_pass1(src.h, float(r), int(complement), None, None, None, 0, ctypes.byref(m), 0)
+    if st not in (DEXEL_OK, DEXEL_EOVERFLOW):
+        _check(st)
+    off = np.empty(src.ncol + 1, dtype=np.uint64)
+    z = np.empty(max(2 * m.value, 2), dtype=np.float32)
+    k = np.empty(max(m.value, 1), dtype=np.uint8)
+    _check(L.dexel_pass1(src.h, float(r), int(complement), off.ctypes.data, z.ctypes.data, k.ctypes.data,
+                         m.value, ctypes.byref(m), 0))
+    return off, z[:2 * m.value], k[:m.value]
+
+
+dilate, erode, shell, pass1 = dexel_dilate, dexel_erode, dexel_shell, dexel_pass1

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars:
+  * pass-1 pieces (selection only): bitwise equal to the oracle's P1;
+  * dilate / erode / shell: identical per-column interval counts after merging
+    gaps < tau and dropping slivers < tau, endpoints within tau, with
+    tau = 1e-4 x spacing (BASELINE.json north_star).
+Small cases compare every column; the big configs C3-C5 compare seeded
+samples of columns (random columns + full rows + full column-lines + the
+first and last rows), in the same launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+import dexelgen as G
+import oracle as O
+from oracle.compare import compare, describe
+
+from tests._util import sample_columns, take_columns
+
+pytestmark = pytest.mark.gpu
+TAU = 1e-4
+
+
+@pytest.fixture(scope="module")
+def dx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_08968_b200 as dx
+    from paper_1804_08968_b200 import build as B
+    B.build()
+    return dx
+
+
+def run_gpu(dx, host, op, r, r2=None):
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    if op == "dilate":
+        dx.dexel_dilate(src, r, dst)
+    elif op == "erode":
+        dx.dexel_erode(src, r, dst)
+    else:
+        dx.dexel_shell(src, r, r if r2 is None else r2, dst)
+    off, ep = dst.download()
+    st = dst.stats()
+    src.close()
+    dst.close()
+    return off, ep, st
+
+
+def run_oracle(host, op, r, r2=None, cols=None):
+    if op == "shell":
+        return O.shell(host, r, r if r2 is None else r2, cols=cols)
+    return getattr(O, op)(host, r, cols=cols)
+
+
+def check(off, ep, ref, cols=None, what=""):
+    if cols is not None:
+        off, ep = take_columns(off, ep, cols)
+    res = compare(off, ep, ref.off, ref.z, TAU)
+    if not res["ok"]:
+        c = res["first_bad"]
+        raise AssertionError(f"{what}: {res}\n" + describe(off, ep, ref.off, ref.z, c))
+    return res
+
+
+# ------------------------------------------------------------------ pass 1 (bitwise)
+@pytest.mark.parametrize("seed", range(40))
+def test_pass1_bitwise_random(dx, seed):
+    rs = np.random.default_rng(seed)
+    nx, ny = int(rs.integers(1, 80)), int(rs.integers(1, 6))
+    host = G.random_grid(nx, ny, 4, -16.0, 16.0, seed, quantum=0.5 if seed % 2 else None)
+    r = float(rs.choice([0.0, 0.7, 1.0, 2.5, 4.0, 9.0, 16.0, 17.0, 33.0, 40.5, 64.0, 100.0, 200.0]))
+    src = dx.Grid.from_host(host)
+    for comp in (False, True):
+        off, z, k = dx.dexel_pass1(src, r, comp)
+        ref = O.pass1(host, r, complement=comp)
+        assert np.array_equal(off, ref.off), (r, comp)
+        assert np.array_equal(z.astype(np.float64), ref.z), (r, comp)
+        assert np.array_equal(k, ref.k), (r, comp)
+
+
+@pytest.mark.parametrize("name,r", [("C1", 3.0), ("C2", 4.0)])
+def test_pass1_bitwise_configs(dx, name, r):
+    host = G.config(name)
+    src = dx.Grid.from_host(host)
+    for comp in (False, True):
+        off, z, k = dx.dexel_pass1(src, r, comp)
+        ref = O.pass1(host, r, complement=comp)
+        assert np.array_equal(off, ref.off) and np.array_equal(z.astype(np.float64), ref.z) \
+            and np.array_equal(k, ref.k)
+
+
+def test_pass1_bitwise_c3_rows(dx):
+    host = G.config("C3")
+    src = dx.Grid.from_host(host)
+    off, z, k = dx.dexel_pass1(src, 8.0)
+    cols = sample_columns(host.nx, host.ny, 4096, 3, 0, 33, extra_rows=(0, host.ny - 1))
+    ref = O.pass1(host, 8.0, cols=cols)
+    o2, z2 = take_columns(off, z, cols)
+    assert np.array_equal(o2, ref.off) and np.array_equal(z2, ref.z)
+    kk = np.concatenate([k[int(off[c]):int(off[c + 1])] for c in cols])
+    assert np.array_equal(kk, ref.k)
+
+
+# ------------------------------------------------------------------ ops, small grids, all columns
+@pytest.mark.parametrize("seed", range(60))
+def test_ops_random_small(dx, seed):
+    rs = np.random.default_rng(1000 + seed)
+    nx, ny = int(rs.integers(1, 40)), int(rs.integers(1, 40))
+    host = G.random_grid(nx, ny, 4, -12.0, 12.0, seed, quantum=0.25 if seed % 3 == 0 else None)
+    r = float(rs.choice([0.0, 0.3, 1.0, 1.5, 2.0, 3.0, 4.0, 5.5, 8.0, 12.0, 20.0]))
+    for op in ("dilate", "erode", "shell"):
+        off, ep, _ = run_gpu(dx, host, op, r, r * 0.75 if op == "shell" else None)
+        ref = run_oracle(host, op, r, r * 0.75 if op == "shell" else None)
+        check(off, ep, ref, what=f"{op} r={r} seed={seed}")
+
+
+@pytest.mark.parametrize("name,r", [("C1", 3.0), ("C2", 4.0)])
+def test_configs_all_columns(dx, name, r):
+    host = G.config(name)
+    for op in G.CONFIGS[name]["op"]:
+        off, ep, _ = run_gpu(dx, host, op, r)
+        check(off, ep, run_oracle(host, op, r), what=f"{name} {op}")
+
+
+# ------------------------------------------------------------------ big configs, sampled columns
+def sampled(dx, name, op, r, n_random=4096, n_rows=2, n_lines=2, seed=7):
+    host = G.config(name)
+    off, ep, st = run_gpu(dx, host, op, r)
+    cols = sample_columns(host.nx, host.ny, n_random, n_rows, n_lines, seed, extra_rows=(0, host.ny - 1))
+    ref = run_oracle(host, op, r, cols=cols)
+    return check(off, ep, ref, cols, what=f"{name} {op} r={r}")
+
+
+@pytest.mark.parametrize("op", ["dilate", "erode"])
+def test_c3_sampled(dx, op):
+    sampled(dx, "C3", op, 8.0)
+
+
+@pytest.mark.parametrize("r", [1.0, 2.0, 4.0, 8.0, 16.0, 32.0, 64.0])
+def test_c4_sampled(dx, r):
+    sampled(dx, "C4", "dilate", r, n_random=2048 if r >= 32 else 4096, n_lines=1)
+
+
+@pytest.mark.slow
+def test_c5_shell_sampled(dx):
+    sampled(dx, "C5", "shell", 16.0, n_random=2048, n_rows=1, n_lines=1)
+
+
+# ------------------------------------------------------------------ edge cases
+def _grid(nx, ny, cols, lo=-8.0, hi=8.0):
+    return G.from_columns(nx, ny, [np.array(c, np.float32).reshape(-1, 2) for c in cols], lo, hi)
+
+
+@pytest.mark.parametrize("op", ["dilate", "erode", "shell"])
+def test_edge_cases(dx, op):
+    cases = [
+        _grid(6, 5, [[]] * 30),                                   # empty
+        _grid(6, 5, [[(-8.0, 8.0)]] * 30),                        # full domain
+        _grid(1, 1, [[(-1.0, 2.0), (3.0, 4.0)]]),                 # single column
+        _grid(7, 3, [[(-8.0, -7.0), (7.5, 8.0)]] * 21),           # touching z_lo / z_hi
+        _grid(5, 5, [[(0.0, 1.0)] if (i + j) % 2 else [(1.0, 2.0)] for j in range(5) for i in range(5)]),  # touching neighbours
+        _grid(40, 2, [[(float(i % 7) - 4, float(i % 7) - 3.5)] for i in range(80)]),
+    ]
+    for host in cases:
+        for r in (0.0, 0.5, 1.0, 2.0, 7.0, 45.0):                 # r = 0, 0<r<1, r > grid size
+            off, ep, _ = run_gpu(dx, host, op, r)
+            check(off, ep, run_oracle(host, op, r), what=f"edge {op} r={r} {host.nx}x{host.ny}")
+
+
+def test_errors(dx):
+    host = _grid(4, 4, [[(0.0, 1.0)]] * 16)
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_dilate(src, -1.0, dst)
+    assert e.value.status == dx.DEXEL_EINVAL
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_dilate(src, 300.0, dst)                          # R > 255
+    assert e.value.status == dx.DEXEL_EINVAL
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_dilate(src, float("nan"), dst)
+    assert e.value.status == dx.DEXEL_EINVAL
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_dilate(src, 1.0, src)
+    assert e.value.status == dx.DEXEL_EINVAL
+    other = dx.Grid(5, 4, -8.0, 8.0)
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_dilate(src, 1.0, other)
+    assert e.value.status == dx.DEXEL_EMISMATCH
+    # corrupt inputs: unsorted, NaN, out of domain, zero length -> EINVAL, grid unchanged
+    before = src.download()
+    for bad in ([(1.0, 0.5)], [(0.0, float("nan"))], [(0.0, 9.0)], [(0.0, 1.0), (0.5, 2.0)], [(1.0, 1.0)]):
+        cols = [[(0.0, 1.0)]] * 15 + [bad]
+        g = _grid(4, 4, [[]] * 16)
+        off = np.zeros(17, np.uint64)
+        np.cumsum([len(c) for c in cols], out=off[1:])
+        ep = np.array([v for c in cols for iv in c for v in iv], np.float32)
+        with pytest.raises(dx.DexelError) as e:
+            src.upload(off, ep)
+        assert e.value.status == dx.DEXEL_EINVAL and "column 15" in str(e.value)
+    after = src.download()
+    assert np.array_equal(before[0], after[0]) and np.array_equal(before[1], after[1])
+    # capacity too small
+    dx.dexel_dilate(src, 1.0, dst)
+    n = dst.size()
+    from paper_1804_08968_b200 import lib
+    offb = np.empty(17, np.uint64)
+    epb = np.empty(2 * n, np.float32)
+    assert lib().dexel_download(dst.h, offb.ctypes.data, epb.ctypes.data, n - 1, 0) == dx.DEXEL_EOVERFLOW
+
+
+def test_deterministic(dx):
+    host = G.config("C2")
+    a = run_gpu(dx, host, "shell", 4.0)
+    b = run_gpu(dx, host, "shell", 4.0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_device_buffers_roundtrip(dx):
+    import torch
+    host = G.config("C1")
+    off = torch.from_numpy(host.off.astype(np.int64)).cuda()
+    ep = torch.from_numpy(host.ep).cuda()
+    src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi)
+    src.upload(off, ep)
+    o2, e2 = src.download(device=True)
+    assert torch.equal(o2.cpu(), off.cpu()) and torch.equal(e2.cpu(), ep.cpu())
+
+
+def test_torch_allocator_hook(dx):
+    dx.use_torch_allocator(True)
+    try:
+        host = G.config("C1")
+        off, ep, _ = run_gpu(dx, host, "dilate", 3.0)
+        check(off, ep, run_oracle(host, "dilate", 3.0), what="torch allocator")
+    finally:
+        dx.use_torch_allocator(False)
