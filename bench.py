@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- dexel columns/s of the separable dexel offset on B200.
+
+Contract:
+  python bench.py --gpus N --steps K --warmup W [--impl b200|reference]
+prints ONE JSON line on rank 0.  A step = one pass of the whole hot path
+(pass 1 with complement-on-load, level sets, pass 2 with the shell epilogue)
+over the workload, default BASELINE.json configs[4] (C5: 4096^2, shell =
+dilate r=16 minus erode r=16) -- the config the 1/2/4/8-GPU metric is quoted
+on.  `--config C4 --op dilate --r 16` selects the 2048^2 dilation workload.
+
+value        output columns / s, whole job, inputs resident in HBM
+e2e          same metric through the C ABI with pinned HOST buffers: H2D of
+             the input CSR + op + D2H of the result inside the timed region
+roofline     dominant kernel: algorithmic bytes / its CUDA-event time, vs
+             MEASURED_PEAKS.json hbm_gbs
+cpu_baseline the fp64 oracle (O2, as it stands) on a bounded band of rows of
+             the same workload, on this host's cores
+--impl reference   times that oracle arm alone (the base contract's reference arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DEFAULT_R = {"C1": 3.0, "C2": 4.0, "C3": 8.0, "C4": 16.0, "C5": 16.0}
+DEFAULT_OP = {"C1": "dilate", "C2": "shell", "C3": "dilate", "C4": "dilate", "C5": "shell"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--op", default=None, choices=[None, "dilate", "erode", "shell"])
+    ap.add_argument("--r", type=float, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=None, help="rows in the oracle band sample")
+    a = ap.parse_args()
+    a.op = a.op or DEFAULT_OP[a.config]
+    a.r = a.r if a.r is not None else DEFAULT_R[a.config]
+    return a
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle arm
+def oracle_band(host, op, r, rows, nthreads):
+    """time the fp64 oracle O2 on a band of full rows in the middle of the grid."""
+    import oracle as O
+    j0 = host.ny // 2 - rows // 2
+    cols = np.arange(j0 * host.nx, (j0 + rows) * host.nx, dtype=np.int64)
+    t = time.perf_counter()
+    if op == "shell":
+        O.shell(host, r, r, cols=cols, nthreads=nthreads)
+    elif op == "erode":
+        O.erode(host, r, cols=cols, nthreads=nthreads)
+    else:
+        O.dilate(host, r, cols=cols, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    return len(cols), dt
+
+
+def default_band_rows(cfg, op, r):
+    # about 10-30 s of CPU work on a 16-core host (oracle O2, measured in the dev container)
+    n = {"C1": 64, "C2": 64, "C3": 16, "C4": 8, "C5": 16}[cfg]
+    if cfg == "C4" and r >= 32:
+        n = 2
+    return n
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def metric_name(op):
+    return f"dexel columns/sec ({op}), whole job"
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    import dexelgen as G
+    host = G.config(a.config)
+    cores = host_cores()
+    rows = a.cpu_rows or max(1, default_band_rows(a.config, a.op, a.r) // 4)
+    for _ in range(a.warmup):
+        oracle_band(host, a.op, a.r, rows, cores)
+    ts, ncols = [], 0
+    for _ in range(a.steps):
+        ncols, dt = oracle_band(host, a.op, a.r, rows, cores)
+        ts.append(dt)
+    tot = sum(ts)
+    v = ncols * len(ts) / tot
+    sample = f"{rows} full rows ({ncols} output columns) from the middle of {a.config} per step"
+    line = {"impl": "reference", "metric": metric_name(a.op), "value": v, "unit": "columns/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * tot / len(ts),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md input recipe)",
+            "config": {"workload": f"{a.config} {a.op} r={a.r}", "grid": f"{host.nx}x{host.ny}", "r": a.r,
+                       "op": a.op, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "columns/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "columns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def algorithmic_bytes(kind, st, ncol, R_list, nfam):
+    """unique HBM bytes the method must move per kernel kind (all launches of one op), DESIGN.md 'Roofline'."""
+    n_in, m, nl, n_out = st["n_in"], st["n_mid"], st["n_lev"], st["n_out"]
+    off = 8 * (ncol + 1)
+    lev_off = sum(8 * ((R + 1) * ncol + 1) for R in R_list)
+    if kind == "pass1_write":   # read S CSR, write pieces (8 B z-pair + 1 B kappa) + read piece offsets
+        return nfam * (off + 8 * n_in + off) + 9 * m
+    if kind == "pass1_count":   # read S CSR, write u32 counts
+        return nfam * (off + 8 * n_in + 4 * ncol)
+    if kind == "levels_write":  # read pieces + offsets, write level intervals + read level offsets
+        return nfam * off + 9 * m + 8 * nl + lev_off
+    if kind == "levels_count":
+        return nfam * off + 9 * m + sum(4 * (R + 1) * ncol for R in R_list)
+    if kind == "pass2_write":   # read level intervals + offsets once, write output + read output offsets
+        return 8 * nl + lev_off + 8 * n_out + off
+    if kind == "pass2_count":
+        return 8 * nl + lev_off + 4 * ncol
+    return 0
+
+
+# ------------------------------------------------------------------ b200 arm
+def run_b200(a, rank, world, local_rank):
+    import torch
+
+    import dexelgen as G
+    import paper_1804_08968_b200 as dx
+    from paper_1804_08968_b200 import build as B
+
+    if not os.path.exists(dx.LIB_PATH):
+        B.build()
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    host = G.config(a.config)
+    ncol = host.ncol
+    stream = torch.cuda.Stream(device=dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        if rank == 0:
+            print(json.dumps({"error": "multi-GPU slab path is not in this build"}), flush=True)
+        sys.exit(2)
+
+    src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi, host.z_ref, 1.0, dev, stream.cuda_stream)
+    src.upload(host.off, host.ep)
+    dst = dx.Grid.like(src)
+
+    def step():
+        if a.op == "dilate":
+            dx.dexel_dilate(src, a.r, dst)
+        elif a.op == "erode":
+            dx.dexel_erode(src, a.r, dst)
+        else:
+            dx.dexel_shell(src, a.r, a.r, dst)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-kernel CUDA events inside the library on the same stream
+    dx.set_timing(True)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    kern_ms = {k: 0.0 for k in dx.KERNEL_NAMES}
+    kern_calls = {k: 0 for k in dx.KERNEL_NAMES}
+    launches = 0
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+        st = dst.stats()
+        launches += st["launches"]
+        for k in dx.KERNEL_NAMES:
+            kern_ms[k] += st["kernel_ms"][k]
+            kern_calls[k] += st["kernel_calls"][k]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dx.set_timing(False)
+    total_ms = e0.elapsed_time(e1)
+    ms = total_ms / a.steps
+    st = dst.stats()
+    value = ncol / (ms / 1e3)
+
+    # ---- roofline for the dominant kernel
+    peak, peak_src = peaks()
+    R = int(np.floor(a.r))
+    nfam = 2 if a.op == "shell" else 1
+    R_list = [R] * nfam
+    dom = max((k for k in dx.KERNEL_NAMES if k not in ("scan", "other")), key=lambda k: kern_ms[k])
+    byts = algorithmic_bytes(dom, st, ncol, R_list, nfam)
+    t_dom = kern_ms[dom] / a.steps / 1e3            # s per step for that kernel kind
+    achieved = byts / t_dom / 1e9 if t_dom > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        key = f"{a.config}:{a.op}:{a.r}:{dom}"
+        traffic = tj.get(key)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_step": byts, "kernel_ms_per_step": 1e3 * t_dom,
+                "kernel_launches_per_step": kern_calls[dom] / a.steps,
+                "share_of_step": (kern_ms[dom] / a.steps) / ms}
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        h_off = torch.from_numpy(host.off.view(np.int64)).pin_memory()
+        h_ep = torch.from_numpy(host.ep).pin_memory()
+        nout_cap = int(st["n_out"] * 1.1) + 1024
+        o_off = torch.empty(ncol + 1, dtype=torch.int64).pin_memory()
+        o_ep = torch.empty(2 * nout_cap, dtype=torch.float32).pin_memory()
+        L = dx.lib()
+        ke = max(1, min(a.steps, 5))
+
+        def e2e_step():
+            dx._check(L.dexel_upload(src.h, h_off.data_ptr(), h_ep.data_ptr(), host.n, 0))
+            step()
+            n = dst.size()
+            dx._check(L.dexel_download(dst.h, o_off.data_ptr(), o_ep.data_ptr(), nout_cap, 0))
+            return n
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(ke):
+            nout = e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ev_ms = e0.elapsed_time(e1) / ke
+        # the library synchronises the stream around host copies, so wall-clock and events agree;
+        # report the larger (host copies are stream-ordered on the same stream)
+        e_ms = max(ev_ms, 1e3 * wall / ke)
+        e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
+               "h2d_bytes_per_step": 8 * (ncol + 1) + 8 * host.n,
+               "d2h_bytes_per_step": 8 * (ncol + 1) + 8 * nout, "ms_per_step": e_ms}
+
+    # ---- cpu baseline (rank 0, N=1 only)
+    cpu = None
+    if not a.no_cpu and rank == 0 and world == 1:
+        cores = host_cores()
+        rows = a.cpu_rows or default_band_rows(a.config, a.op, a.r)
+        ncols_s, dt = oracle_band(host, a.op, a.r, rows, cores)
+        cpu = {"value": ncols_s / dt, "unit": "columns/s", "cores": cores, "kind": "oracle",
+               "sample": f"O2 fp64 oracle on {rows} full rows ({ncols_s} output columns) from the middle of "
+                         f"{a.config}, {dt:.1f} s"}
+
+    line = {
+        "metric": metric_name(a.op), "value": value, "unit": "columns/s", "n_gpus": world, "steps": a.steps,
+        "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator, DESIGN.md input recipe)",
+        "config": {"workload": f"{a.config} {a.op} r={a.r}", "grid": f"{host.nx}x{host.ny}", "r": a.r,
+                   "op": a.op, "n_in": int(st["n_in"]), "n_mid": int(st["n_mid"]), "n_lev": int(st["n_lev"]),
+                   "n_out": int(st["n_out"]), "parallelism": f"y-slabs x{world}",
+                   "l2": f"inputs larger than L2 ({8 * host.n / 2**20:.0f} MiB endpoints + intermediates)"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "gpu_launches_per_step": launches / a.steps, "clocks": clk,
+        "kernel_ms_per_step": {k: v / a.steps for k, v in kern_ms.items()},
+        "gpu": torch.cuda.get_device_name(dev),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+    else:
+        run_b200(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

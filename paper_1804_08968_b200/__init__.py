@@ -25,7 +25,7 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
-           "dexel_set_allocator", "dexel_last_stats"]
+           "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing"]
 
 
 class DexelError(RuntimeError):
@@ -42,9 +42,15 @@ class dexel_desc(ctypes.Structure):
                 ("y1", ctypes.c_int32)]
 
 
+NKERNELS = 8
+KERNEL_NAMES = ["pass1_count", "pass1_write", "levels_count", "levels_write", "pass2_count", "pass2_write",
+                "scan", "other"]
+
+
 class dexel_stats(ctypes.Structure):
     _fields_ = [("n_in", ctypes.c_uint64), ("n_mid", ctypes.c_uint64), ("n_lev", ctypes.c_uint64),
-                ("n_out", ctypes.c_uint64), ("stage_ms", ctypes.c_float * 4)]
+                ("n_out", ctypes.c_uint64), ("launches", ctypes.c_uint32),
+                ("kernel_calls", ctypes.c_uint32 * NKERNELS), ("kernel_ms", ctypes.c_float * NKERNELS)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
@@ -75,6 +81,7 @@ def lib():
             "dexel_last_error": ([], ctypes.c_char_p),
             "dexel_set_allocator": ([ALLOC_FN, FREE_FN, vp], ctypes.c_int),
             "dexel_last_stats": ([vp, ctypes.POINTER(dexel_stats)], ctypes.c_int),
+            "dexel_set_timing": ([ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -187,7 +194,9 @@ class Grid:
     def stats(self) -> dict:
         s = dexel_stats()
         _check(lib().dexel_last_stats(self.h, ctypes.byref(s)))
-        return dict(n_in=s.n_in, n_mid=s.n_mid, n_lev=s.n_lev, n_out=s.n_out, stage_ms=list(s.stage_ms))
+        return dict(n_in=s.n_in, n_mid=s.n_mid, n_lev=s.n_lev, n_out=s.n_out, launches=s.launches,
+                    kernel_calls=dict(zip(KERNEL_NAMES, list(s.kernel_calls))),
+                    kernel_ms=dict(zip(KERNEL_NAMES, list(s.kernel_ms))))
 
     def sync(self):
         _check(lib().dexel_sync(self.h))
@@ -202,6 +211,11 @@ class Grid:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def set_timing(on: bool):
+    """per-kernel CUDA-event timing inside the library (dexel_set_timing)."""
+    _check(lib().dexel_set_timing(1 if on else 0))
 
 
 # ---------------------------------------------------------------- operations (same names as the C ABI)

@@ -24,6 +24,8 @@ namespace {
 
 thread_local std::string g_err;
 
+bool g_timing = false;
+
 dexel_alloc_fn g_alloc = nullptr;
 dexel_free_fn g_free = nullptr;
 void* g_alloc_ctx = nullptr;
@@ -85,12 +87,57 @@ void dfree(dexel_grid g, Buf& b) {
   b.bytes = 0;
 }
 
+// per-op kernel accounting: launch counts always, CUDA-event device times when g_timing
+enum { K_P1C = 0, K_P1W = 1, K_LVC = 2, K_LVW = 3, K_P2C = 4, K_P2W = 5, K_SCAN = 6, K_OTHER = 7 };
+struct Prof {
+  cudaStream_t st = nullptr;
+  dexel_stats* s = nullptr;
+  bool on = false;
+  int curk = K_OTHER;
+  cudaEvent_t cur = nullptr;
+  struct Rec { int k; cudaEvent_t a, b; };
+  std::vector<Rec> ev;
+  void pre(int k) {
+    curk = k;
+    if (on) { cudaEventCreate(&cur); cudaEventRecord(cur, st); }
+  }
+  void post() {
+    if (s) { s->launches++; s->kernel_calls[curk]++; }
+    if (on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      ev.push_back({curk, cur, e});
+    }
+  }
+  void finish() {
+    if (!ev.empty()) {
+      cudaEventSynchronize(ev.back().b);
+      for (auto& r : ev) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        if (s) s->kernel_ms[r.k] += ms;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+      }
+      ev.clear();
+    }
+  }
+  ~Prof() { finish(); }
+};
+
 // RAII for temporaries of one op
 struct Temps {
   dexel_grid g;
   std::vector<Buf> bufs;
-  explicit Temps(dexel_grid g_) : g(g_) {}
+  Prof prof;
+  explicit Temps(dexel_grid g_, dexel_stats* st = nullptr) : g(g_) {
+    prof.st = g_->stream;
+    prof.s = st;
+    prof.on = g_timing && st != nullptr;
+  }
   ~Temps() {
+    prof.finish();
     for (auto& b : bufs) dfree(g, b);
   }
   dexel_status get(size_t bytes, void** p) {
@@ -107,6 +154,8 @@ struct Temps {
   }
 };
 
+#define LAUNCH(T, KID, ...) do { (T).prof.pre(KID); __VA_ARGS__; (T).prof.post(); } while (0)
+
 // exclusive scan of cnt[0..n) into off[0..n], returns total (synchronising read)
 dexel_status scan_counts(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n, uint64_t* off, uint64_t* total) {
   const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -119,9 +168,9 @@ dexel_status scan_counts(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n
     T.release(sums);
     return DEXEL_OK;
   }
-  scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums);
-  scan_sums_exclusive<<<1, SCAN_THREADS, 0, g->stream>>>(sums, ntiles);
-  scan_tiles_write<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums, off);
+  LAUNCH(T, K_SCAN, scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums));
+  LAUNCH(T, K_SCAN, scan_sums_exclusive<<<1, SCAN_THREADS, 0, g->stream>>>(sums, ntiles));
+  LAUNCH(T, K_SCAN, scan_tiles_write<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums, off));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(total, off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
@@ -174,13 +223,13 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
   dexel_status s;
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&cnt))) return s;
   if ((s = T.get(sizeof(uint64_t) * (ncol + 1), (void**)&P->moff))) return s;
-  launch_pass1<false>(NW, src, R, complement, row0, nrows_out, cnt, nullptr, nullptr, nullptr, g->stream);
+  LAUNCH(T, K_P1C, launch_pass1<false>(NW, src, R, complement, row0, nrows_out, cnt, nullptr, nullptr, nullptr, g->stream));
   CK(cudaGetLastError());
   if ((s = scan_counts(g, T, cnt, (uint64_t)ncol, P->moff, &P->m))) return s;
   T.release(cnt);
   if ((s = T.get(sizeof(float2) * (P->m + 1), (void**)&P->mz))) return s;
   if ((s = T.get(P->m + 16, (void**)&P->mk))) return s;
-  launch_pass1<true>(NW, src, R, complement, row0, nrows_out, nullptr, P->moff, P->mz, P->mk, g->stream);
+  LAUNCH(T, K_P1W, launch_pass1<true>(NW, src, R, complement, row0, nrows_out, nullptr, P->moff, P->mz, P->mk, g->stream));
   CK(cudaGetLastError());
   return DEXEL_OK;
 }
@@ -226,8 +275,8 @@ dexel_status make_tables(dexel_grid g, Temps& T, float r, int R, LevelTables* L)
 }
 
 template <bool WRITE>
-void launch_levels(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* sz, const LevelTables& L, float zlo,
-                   float zhi, uint32_t* lcnt, const uint64_t* loff, float2* lz, cudaStream_t st) {
+void launch_levels_envelope(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* sz, const LevelTables& L,
+                            float zlo, float zhi, uint32_t* lcnt, const uint64_t* loff, float2* lz, cudaStream_t st) {
   const unsigned blocks = (unsigned)((ncol + 127) / 128);
   if (blocks == 0) return;
 #define LV(ML) levels_kernel<ML, WRITE><<<blocks, 128, 0, st>>>(ncol, P.moff, P.mz, P.mk, sp, sz, L, zlo, zhi, lcnt, loff, lz)
@@ -236,6 +285,49 @@ void launch_levels(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* s
   else if (R + 1 <= 128) LV(128);
   else LV(256);
 #undef LV
+}
+
+template <int NS, bool WRITE>
+void launch_levels2_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
+                      uint32_t* lcnt, const uint64_t* loff, float2* lz, int* ovf, cudaStream_t st) {
+  constexpr int WARPS = LvCfg<NS>::WARPS;
+  const int nl = R + 1;
+  const int G = NS == 1 ? 32 / nl : 1;
+  const int h_in_smem = nl * nl <= 8192 ? 1 : 0;
+  const size_t smem = sizeof(float2) * WARPS * NS * LV_D * 32 + (h_in_smem ? sizeof(float) * nl * nl : 0);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(levels2_kernel<NS, WRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  const int64_t per_block = (int64_t)WARPS * G;
+  const unsigned blocks = (unsigned)((ncol + per_block - 1) / per_block);
+  if (blocks == 0) return;
+  levels2_kernel<NS, WRITE><<<blocks, WARPS * 32, smem, st>>>(ncol, P.moff, P.mz, P.mk, L.h, R, h_in_smem, zlo,
+                                                                 zhi, lcnt, loff, lz, ovf);
+}
+
+bool levels_envelope_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DEXEL_LEVELS");
+    v = (e && std::strcmp(e, "envelope") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <bool WRITE>
+void launch_levels(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* sz, const LevelTables& L, float zlo,
+                   float zhi, uint32_t* lcnt, const uint64_t* loff, float2* lz, int* ovf, cudaStream_t st) {
+  if (levels_envelope_mode()) {
+    launch_levels_envelope<WRITE>(R, ncol, P, sp, sz, L, zlo, zhi, lcnt, loff, lz, st);
+    return;
+  }
+  const int nl = R + 1;
+  if (nl <= 32) launch_levels2_t<1, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
+  else if (nl <= 64) launch_levels2_t<2, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
+  else if (nl <= 128) launch_levels2_t<4, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
+  else launch_levels2_t<8, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
 }
 
 // one dilation family: rows [row0, row0+nrows) of src (S or its complement) at radius r
@@ -254,21 +346,32 @@ dexel_status run_family(dexel_grid g, Temps& T, const SrcRows& src, float r, int
   double* sz = nullptr;
   uint64_t* loff = nullptr;
   float2* lz = nullptr;
+  int* ovf = nullptr;
   const uint64_t nl = (uint64_t)(R + 1) * (uint64_t)ncol;
-  if ((s = T.get(sizeof(uint32_t) * (P.m + 1), (void**)&sp))) return s;
-  if ((s = T.get(sizeof(double) * (P.m + 1), (void**)&sz))) return s;
+  if (levels_envelope_mode()) {
+    if ((s = T.get(sizeof(uint32_t) * (P.m + 1), (void**)&sp))) return s;
+    if ((s = T.get(sizeof(double) * (P.m + 1), (void**)&sz))) return s;
+  }
+  if ((s = T.get(sizeof(int) * 4, (void**)&ovf))) return s;
+  CK(cudaMemsetAsync(ovf, 0, sizeof(int), g->stream));
   if ((s = T.get(sizeof(uint32_t) * (nl + 1), (void**)&lcnt))) return s;
   if ((s = T.get(sizeof(uint64_t) * (nl + 1), (void**)&loff))) return s;
-  launch_levels<false>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, lcnt, nullptr, nullptr, g->stream);
+  LAUNCH(T, K_LVC, launch_levels<false>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, lcnt, nullptr, nullptr, ovf, g->stream));
   CK(cudaGetLastError());
   uint64_t nlev = 0;
   if ((s = scan_counts(g, T, lcnt, nl, loff, &nlev))) return s;
   T.release(lcnt);
+  int hovf = 0;
+  CK(cudaMemcpyAsync(&hovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  if (hovf)
+    return fail(DEXEL_EOVERFLOW, "more than " + std::to_string(LV_D) +
+                                     " open union intervals of one level within the growth window of a column");
   if ((s = T.get(sizeof(float2) * (nlev + 1), (void**)&lz))) return s;
-  launch_levels<true>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, nullptr, loff, lz, g->stream);
+  LAUNCH(T, K_LVW, launch_levels<true>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, nullptr, loff, lz, ovf, g->stream));
   CK(cudaGetLastError());
-  T.release(sp);
-  T.release(sz);
+  if (sp) T.release(sp);
+  if (sz) T.release(sz);
   T.release(P.mz);
   T.release(P.mk);
   T.release(P.moff);
@@ -310,15 +413,6 @@ void set_empty(dexel_grid g) {
   g->n = 0;
 }
 
-bool stage_timing() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("DEXEL_STAGE_TIMING");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
   if (src == dst) return fail(DEXEL_EINVAL, "src and dst must be different handles");
@@ -337,18 +431,12 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
     CK(cudaStreamWaitEvent(st, ev, 0));
     cudaEventDestroy(ev);
   }
-  cudaEvent_t evs[4];
-  const bool timing = stage_timing();
-  if (timing)
-    for (auto& e : evs) cudaEventCreate(&e);
-
-  Temps T(src);
+  dexel_stats stats{};
+  Temps T(src, &stats);
   SrcRows rows{(const uint64_t*)src->off.p, (const float*)src->ep.p, src->d.nx, src->nrows, src->d.z_lo,
                src->d.z_hi};
-  dexel_stats stats{};
   stats.n_in = src->n;
   Family FA, FB;
-  if (timing) cudaEventRecord(evs[0], st);
   // family A: dilate S (dilate, shell r_out) or C (erode)
   if ((s = run_family(src, T, rows, r_a, op == OP_ERODE ? 1 : 0, 0, src->nrows, &FA, &stats.n_mid))) {
     set_empty(dst);
@@ -364,7 +452,6 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   } else {
     FB = FA;
   }
-  if (timing) cudaEventRecord(evs[1], st);
   // pass 2
   const int64_t ncol = src->ncol;
   uint32_t* ocnt = nullptr;
@@ -372,8 +459,8 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
   if ((s = T.get(sizeof(int) * 4, (void**)&ovf))) return s;
   CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-  launch_pass2<false>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, ocnt, nullptr, nullptr,
-                      ovf, st);
+  LAUNCH(T, K_P2C, launch_pass2<false>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, ocnt,
+                                       nullptr, nullptr, ovf, st));
   CK(cudaGetLastError());
   uint64_t nout = 0;
   // dst offsets: reuse dst->off
@@ -388,18 +475,12 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   }
   dfree(dst, dst->ep);
   if ((s = dalloc(dst, dst->ep, sizeof(float2) * (nout + 1)))) return s;
-  launch_pass2<true>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, nullptr,
-                     (const uint64_t*)dst->off.p, (float2*)dst->ep.p, ovf, st);
+  LAUNCH(T, K_P2W, launch_pass2<true>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, nullptr,
+                                      (const uint64_t*)dst->off.p, (float2*)dst->ep.p, ovf, st));
   CK(cudaGetLastError());
   dst->n = nout;
   stats.n_out = nout;
-  if (timing) {
-    cudaEventRecord(evs[2], st);
-    cudaEventSynchronize(evs[2]);
-    cudaEventElapsedTime(&stats.stage_ms[0], evs[0], evs[1]);
-    cudaEventElapsedTime(&stats.stage_ms[1], evs[1], evs[2]);
-    for (auto& e : evs) cudaEventDestroy(e);
-  }
+  T.prof.finish();
   if (dst->stream != st) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -438,6 +519,18 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
   if (d->y0 < 0 || d->y1 > d->ny || d->y0 >= d->y1) return fail(DEXEL_EINVAL, "bad slab rows [y0,y1)");
   if (d->nranks == 1 && (d->y0 != 0 || d->y1 != d->ny)) return fail(DEXEL_EINVAL, "single rank must own all rows");
   CK(cudaSetDevice(d->device));
+  {
+    // keep freed pool memory mapped: ops allocate and free tens of GB per call
+    static bool pool_set[64] = {false};
+    if (d->device >= 0 && d->device < 64 && !pool_set[d->device]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set[d->device] = true;
+    }
+  }
   dexel_grid g = new dexel_grid_s();
   g->d = *d;
   g->nrows = d->y1 - d->y0;
@@ -592,6 +685,11 @@ void dexel_destroy(dexel_grid g) {
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
+}
+
+dexel_status dexel_set_timing(int on) {
+  g_timing = on != 0;
+  return DEXEL_OK;
 }
 
 dexel_status dexel_last_stats(dexel_grid g, dexel_stats* out) {

@@ -381,6 +381,127 @@ __global__ void __launch_bounds__(128) levels_kernel(int64_t ncol, const uint64_
     for (int k = 0; k <= R; ++k) lcnt[(int64_t)k * ncol + c] = st.ncnt[k];
 }
 
+// ------------------------------------------------------------------ levels (lanes = levels)
+// Same result as levels_kernel, organised for SIMT throughput: a warp owns G
+// columns (G = 32 / (R+1) for R < 32, else 1) and lane (g, k) builds the
+// superlevel set L_k of column g directly as the union of the grown pieces
+//   L_k = U_{p : kappa_p^2 + k^2 <= (r/s)^2} [lo_p - h(kappa_p,k), hi_p + h(kappa_p,k)]
+// (capsule of PAPER.md:538-541 restricted to the row at lateral distance k).
+// Pieces are read coalesced, L lanes at a time, and broadcast with shuffles;
+// each lane keeps a small deque of not-yet-final union intervals in shared
+// memory: an interval whose end is below lo - h(0,k) can no longer grow
+// (every later piece starts at >= lo and grows by <= h(0,k)), so it is emitted.
+constexpr int LV_D = 16;   // deque depth per lane and level slot
+
+template <int NS>
+struct LvCfg {
+  static constexpr int WARPS = NS <= 2 ? 4 : (NS == 4 ? 2 : 1);
+};
+
+template <int NS, bool WRITE>
+__global__ void __launch_bounds__(LvCfg<NS>::WARPS * 32) levels2_kernel(
+    int64_t ncol, const uint64_t* __restrict__ moff, const float2* __restrict__ mz, const uint8_t* __restrict__ mk,
+    const float* __restrict__ htab, int R, int h_in_smem, float zlo, float zhi, uint32_t* __restrict__ lcnt,
+    const uint64_t* __restrict__ loff, float2* __restrict__ lz, int* __restrict__ overflow) {
+  constexpr int WARPS = LvCfg<NS>::WARPS;
+  extern __shared__ float4 lv_smem4[];
+  float2* dq_all = reinterpret_cast<float2*>(lv_smem4);                 // [WARPS][NS][LV_D][32]
+  float* hs = reinterpret_cast<float*>(dq_all + WARPS * NS * LV_D * 32);  // [(R+1)^2] if h_in_smem
+  const int L = R + 1;
+  if (h_in_smem) {
+    for (int t = threadIdx.x; t < L * L; t += blockDim.x) hs[t] = htab[t];
+    __syncthreads();
+  }
+  const float* H = h_in_smem ? hs : htab;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = NS == 1 ? 32 / L : 1;           // columns per warp (L <= 32 when NS == 1)
+  const int LC = NS == 1 ? L : 32;              // lanes per column group
+  const int g = lane / LC, u0 = lane % LC;
+  const bool lane_ok = g < G;
+  const int64_t c = ((int64_t)blockIdx.x * WARPS + wib) * G + g;
+  const bool col_ok = lane_ok && c < ncol;
+  float2* dq = dq_all + (size_t)wib * NS * LV_D * 32;
+
+  uint64_t base = 0;
+  uint32_t m = 0;
+  if (col_ok) { base = moff[c]; m = (uint32_t)(moff[c + 1] - base); }
+  int kk[NS], b[NS], n[NS];
+  uint32_t cnt[NS];
+  float Hk[NS];
+  uint64_t obase[NS];
+  bool ovf = false;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    kk[s] = u0 + 32 * s;
+    b[s] = 0; n[s] = 0; cnt[s] = 0; obase[s] = 0;
+    const bool v = col_ok && kk[s] <= R;
+    Hk[s] = v ? H[kk[s]] : 0.f;                  // h(0,k): the largest growth at level k
+    if (WRITE && v) obase[s] = loff[(int64_t)kk[s] * ncol + c];
+  }
+  auto emit = [&](int s, float2 iv) {
+    const float lo = fmaxf(iv.x, zlo), hi = fminf(iv.y, zhi);
+    if (lo < hi) {
+      if (WRITE) lz[obase[s] + cnt[s]] = make_float2(lo, hi);
+      ++cnt[s];
+    }
+  };
+  const uint32_t mmax = __reduce_max_sync(FULL, m);
+  for (uint32_t t0 = 0; t0 < mmax; t0 += LC) {
+    float2 pz = make_float2(0.f, 0.f);
+    int pk = 0;
+    if (t0 + u0 < m) { pz = mz[base + t0 + u0]; pk = mk[base + t0 + u0]; }
+    const int nu = min((uint32_t)LC, mmax - t0);
+    for (int u = 0; u < nu; ++u) {
+      const int srcl = g * LC + u;
+      const float lo = __shfl_sync(FULL, pz.x, srcl);
+      const float hi = __shfl_sync(FULL, pz.y, srcl);
+      const int kap = __shfl_sync(FULL, pk, srcl);
+      if (t0 + u >= m) continue;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (kk[s] > R) continue;
+        float2* q = dq + (size_t)s * LV_D * 32 + lane;   // q[d*32]
+        const float lim = lo - Hk[s];
+        while (n[s] > 0 && q[b[s] * 32].y < lim) {      // final: cannot be reached by later pieces
+          emit(s, q[b[s] * 32]);
+          b[s] = (b[s] + 1) & (LV_D - 1);
+          --n[s];
+        }
+        const float hv = H[kap * L + kk[s]];
+        if (hv >= 0.f) {
+          float s0 = lo - hv, e0 = hi + hv;
+          while (n[s] > 0) {
+            const int top = (b[s] + n[s] - 1) & (LV_D - 1);
+            const float2 tv = q[top * 32];
+            if (tv.y < s0) break;
+            s0 = fminf(s0, tv.x);
+            e0 = fmaxf(e0, tv.y);
+            --n[s];
+          }
+          if (n[s] == LV_D) {
+            ovf = true;
+          } else {
+            q[((b[s] + n[s]) & (LV_D - 1)) * 32] = make_float2(s0, e0);
+            ++n[s];
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (!col_ok || kk[s] > R) continue;
+    float2* q = dq + (size_t)s * LV_D * 32 + lane;
+    while (n[s] > 0) {
+      emit(s, q[b[s] * 32]);
+      b[s] = (b[s] + 1) & (LV_D - 1);
+      --n[s];
+    }
+    if (!WRITE) lcnt[(int64_t)kk[s] * ncol + c] = cnt[s];
+  }
+  if (ovf) atomicExch(overflow, 1);
+}
+
 // ------------------------------------------------------------------ pass 2
 struct LevelFamily {
   const uint64_t* loff;  // [(R+1)*ncol + 1], level-major

@@ -238,3 +238,27 @@ def test_torch_allocator_hook(dx):
         check(off, ep, run_oracle(host, "dilate", 3.0), what="torch allocator")
     finally:
         dx.use_torch_allocator(False)
+
+
+def test_levels_envelope_variant_matches(dx):
+    """The alternative level-set kernel (explicit upper envelope F, DEXEL_LEVELS=envelope)
+    agrees with the oracle too: run it in a subprocess (the mode is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
+from oracle.compare import compare
+for seed in range(12):
+    rs = np.random.default_rng(77 + seed)
+    host = G.random_grid(int(rs.integers(2, 30)), int(rs.integers(2, 30)), 4, -12.0, 12.0, seed)
+    r = float(rs.choice([1.0, 2.5, 4.0, 7.0]))
+    src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
+    dx.dexel_erode(src, r, dst); off, ep = dst.download(); ref = O.erode(host, r)
+    res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], res
+print("OK")
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DEXEL_LEVELS="envelope")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
