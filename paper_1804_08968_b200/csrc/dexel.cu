@@ -57,6 +57,7 @@ struct dexel_grid_s {
   Buf off, ep;
   uint64_t n = 0;
   dexel_stats stats{};
+  double lev_ratio = 0.0;   // n_lev / n_mid of the last op (arena sizing hint)
 };
 
 namespace {
@@ -240,94 +241,99 @@ struct Family {
   uint64_t nlev = 0;
 };
 
-dexel_status make_tables(dexel_grid g, Temps& T, float r, int R, LevelTables* L) {
+dexel_status make_tables(dexel_grid g, Temps& T, float r, int R, LevelTables* L, EnvTables* E) {
   const double s = g->d.spacing;
   const int n1 = R + 1;
-  std::vector<double> W(n1), Tk(n1);
   std::vector<float> h((size_t)n1 * n1);
+  std::vector<double> W(n1), Tk(n1);
   const double rr = (double)r * (double)r;
-  for (int k = 0; k < n1; ++k) {
-    W[k] = rr - (double)k * k * s * s;
-    Tk[k] = (double)k * k * s * s;
+  for (int a = 0; a < n1; ++a) {
+    W[a] = rr - (double)a * a * s * s;
+    Tk[a] = (double)a * a * s * s;
   }
   for (int a = 0; a < n1; ++a)
     for (int k = 0; k < n1; ++k) {
+      // W(kappa) - T(k) in fp64, rounded once to fp32; valid iff T(k) <= W(kappa)
       const double w = W[a] - Tk[k];
       h[(size_t)a * n1 + k] = w >= 0.0 ? (float)std::sqrt(w) : -1.0f;
     }
-  void* buf = nullptr;
-  const size_t bytes = sizeof(double) * 2 * n1 + sizeof(float) * h.size();
+  char* buf = nullptr;
+  const size_t hb = sizeof(float) * h.size(), db = sizeof(double) * n1;
   dexel_status st;
-  if ((st = T.get(bytes, &buf))) return st;
+  if ((st = T.get(hb + 2 * db + 64, (void**)&buf))) return st;
   double* dW = (double*)buf;
   double* dT = dW + n1;
   float* dh = (float*)(dT + n1);
-  CK(cudaMemcpyAsync(dW, W.data(), sizeof(double) * n1, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(dT, Tk.data(), sizeof(double) * n1, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(dh, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(dW, W.data(), db, cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(dT, Tk.data(), db, cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(dh, h.data(), hb, cudaMemcpyHostToDevice, g->stream));
   CK(cudaStreamSynchronize(g->stream));  // host vectors go out of scope
-  L->Wp = dW;
-  L->T = dT;
   L->h = dh;
   L->R = R;
-  L->inv_s2 = 1.0 / (s * s);
+  E->h = dh;
+  E->W = dW;
+  E->Tk = dT;
+  E->R = R;
+  E->r = (double)r;
+  E->inv_s2 = 1.0 / (s * s);
   return DEXEL_OK;
 }
 
-template <bool WRITE>
-void launch_levels_envelope(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* sz, const LevelTables& L,
-                            float zlo, float zhi, uint32_t* lcnt, const uint64_t* loff, float2* lz, cudaStream_t st) {
-  const unsigned blocks = (unsigned)((ncol + 127) / 128);
-  if (blocks == 0) return;
-#define LV(ML) levels_kernel<ML, WRITE><<<blocks, 128, 0, st>>>(ncol, P.moff, P.mz, P.mk, sp, sz, L, zlo, zhi, lcnt, loff, lz)
-  if (R + 1 <= 8) LV(8);
-  else if (R + 1 <= 32) LV(32);
-  else if (R + 1 <= 128) LV(128);
-  else LV(256);
-#undef LV
-}
-
-template <int NS, bool WRITE>
-void launch_levels2_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
-                      uint32_t* lcnt, const uint64_t* loff, float2* lz, int* ovf, cudaStream_t st) {
-  constexpr int WARPS = LvCfg<NS>::WARPS;
+template <int NS>
+void launch_levels4_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
+                      const LevelOut& O, cudaStream_t st) {
+  constexpr int WARPS = Lv4Cfg<NS>::WARPS;
   const int nl = R + 1;
   const int G = NS == 1 ? 32 / nl : 1;
-  const int h_in_smem = nl * nl <= 8192 ? 1 : 0;
-  const size_t smem = sizeof(float2) * WARPS * NS * LV_D * 32 + (h_in_smem ? sizeof(float) * nl * nl : 0);
+  const int h_in_smem = sizeof(float) * nl * nl <= 64 * 1024 ? 1 : 0;
+  const size_t smem = sizeof(float2) * WARPS * 2 * NS * STG_C * 32 + (h_in_smem ? sizeof(float) * nl * nl : 0);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(levels2_kernel<NS, WRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(levels4_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   const int64_t per_block = (int64_t)WARPS * G;
   const unsigned blocks = (unsigned)((ncol + per_block - 1) / per_block);
   if (blocks == 0) return;
-  levels2_kernel<NS, WRITE><<<blocks, WARPS * 32, smem, st>>>(ncol, P.moff, P.mz, P.mk, L.h, R, h_in_smem, zlo,
-                                                                 zhi, lcnt, loff, lz, ovf);
+  levels4_kernel<NS><<<blocks, WARPS * 32, smem, st>>>(ncol, P.moff, P.mz, P.mk, L, h_in_smem, zlo, zhi, O);
 }
 
-bool levels_envelope_mode() {
+template <int LMAX>
+void launch_levels5_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
+                      const LevelOut& O, cudaStream_t st) {
+  (void)R;
+  const unsigned blocks = (unsigned)((ncol + 127) / 128);
+  if (blocks == 0) return;
+  levels5_kernel<LMAX><<<blocks, 128, 0, st>>>(ncol, P.moff, P.mz, P.mk, L, zlo, zhi, O);
+}
+
+void launch_levels(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
+                   const LevelOut& O, cudaStream_t st) {
+  const int nl = R + 1;
+  // R < 17: one thread per column, 2(R+1) running unions in registers (levels5);
+  // larger R: one warp per column, lanes = levels (levels4)
+  if (nl <= 2) launch_levels5_t<2>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 3) launch_levels5_t<3>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 5) launch_levels5_t<5>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 9) launch_levels5_t<9>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 17) launch_levels5_t<17>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 32) launch_levels4_t<1>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 64) launch_levels4_t<2>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 96) launch_levels4_t<3>(R, ncol, P, L, zlo, zhi, O, st);
+  else if (nl <= 128) launch_levels4_t<4>(R, ncol, P, L, zlo, zhi, O, st);
+  else launch_levels4_t<8>(R, ncol, P, L, zlo, zhi, O, st);
+}
+
+// level-set kernel: 1 = per-level running unions (levels5 for R < 17, levels4 above;
+// default), 0 = power-diagram envelope (levels6; DEXEL_LEVELS=envelope, cross-checked
+// in tests)
+int levels_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("DEXEL_LEVELS");
-    v = (e && std::strcmp(e, "envelope") == 0) ? 1 : 0;
+    v = (e && std::strcmp(e, "envelope") == 0) ? 0 : 1;
   }
-  return v == 1;
-}
-
-template <bool WRITE>
-void launch_levels(int R, int64_t ncol, const Pieces& P, uint32_t* sp, double* sz, const LevelTables& L, float zlo,
-                   float zhi, uint32_t* lcnt, const uint64_t* loff, float2* lz, int* ovf, cudaStream_t st) {
-  if (levels_envelope_mode()) {
-    launch_levels_envelope<WRITE>(R, ncol, P, sp, sz, L, zlo, zhi, lcnt, loff, lz, st);
-    return;
-  }
-  const int nl = R + 1;
-  if (nl <= 32) launch_levels2_t<1, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
-  else if (nl <= 64) launch_levels2_t<2, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
-  else if (nl <= 128) launch_levels2_t<4, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
-  else launch_levels2_t<8, WRITE>(R, ncol, P, L, zlo, zhi, lcnt, loff, lz, ovf, st);
+  return v;
 }
 
 // one dilation family: rows [row0, row0+nrows) of src (S or its complement) at radius r
@@ -340,48 +346,62 @@ dexel_status run_family(dexel_grid g, Temps& T, const SrcRows& src, float r, int
   if ((s = run_pass1(g, T, src, R, complement, row0, nrows, &P))) return s;
   *n_mid += P.m;
   LevelTables L;
-  if ((s = make_tables(g, T, r, R, &L))) return s;
+  EnvTables E;
+  if ((s = make_tables(g, T, r, R, &L, &E))) return s;
   const int64_t ncol = (int64_t)nrows * src.nx;
-  uint32_t *sp = nullptr, *lcnt = nullptr;
-  double* sz = nullptr;
-  uint64_t* loff = nullptr;
-  float2* lz = nullptr;
-  int* ovf = nullptr;
-  const uint64_t nl = (uint64_t)(R + 1) * (uint64_t)ncol;
-  if (levels_envelope_mode()) {
-    if ((s = T.get(sizeof(uint32_t) * (P.m + 1), (void**)&sp))) return s;
-    if ((s = T.get(sizeof(double) * (P.m + 1), (void**)&sz))) return s;
+  const int ndir = levels_mode() == 0 ? 1 : 2;
+  const int ntask = ndir * (R + 1);
+  LevelOut O;
+  if ((s = T.get(sizeof(uint64_t) * (ncol + 1), (void**)&O.dbase))) return s;
+  if ((s = T.get(sizeof(uint32_t) * (ncol * (ntask + 1) + 1), (void**)&O.rel))) return s;
+  if ((s = T.get(sizeof(unsigned long long) * 2, (void**)&O.counter))) return s;
+  // arena sized from the previous op's level/piece ratio (rerun with the exact size if it overflows)
+  const double ratio = g->lev_ratio > 0 ? g->lev_ratio * 1.1 : 1.5;
+  O.cap = (uint64_t)(ratio * (double)P.m) + 4096;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if ((s = T.get(sizeof(float2) * (O.cap + 1), (void**)&O.arena))) return s;
+    CK(cudaMemsetAsync(O.counter, 0, 2 * sizeof(unsigned long long), g->stream));
+    if (ndir == 1) {
+      const size_t smem = (sizeof(float) + sizeof(uint32_t)) * (R + 1) * 128;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(levels6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const unsigned blocks = (unsigned)((ncol + 127) / 128);
+      if (blocks) LAUNCH(T, K_LVW, levels6_kernel<<<blocks, 128, smem, g->stream>>>(ncol, P.moff, P.mz, P.mk, E,
+                                                                                    src.zlo, src.zhi, O));
+    } else {
+      LAUNCH(T, K_LVW, launch_levels(R, ncol, P, L, src.zlo, src.zhi, O, g->stream));
+    }
+    CK(cudaGetLastError());
+    unsigned long long used2[2] = {0, 0};
+    CK(cudaMemcpyAsync(used2, O.counter, sizeof(used2), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const unsigned long long used = used2[0];
+    if (used2[1])
+      return fail(DEXEL_EOVERFLOW, ndir == 1 ? "a column's power-diagram envelope exceeds the deque capacity"
+                                             : "a column has more than 65534 intervals in one level list");
+    if (used <= O.cap) {
+      out->nlev = used;
+      break;
+    }
+    T.release(O.arena);
+    O.cap = used;
+    if (attempt == 1) return fail(DEXEL_ECUDA, "level arena sizing did not converge");
   }
-  if ((s = T.get(sizeof(int) * 4, (void**)&ovf))) return s;
-  CK(cudaMemsetAsync(ovf, 0, sizeof(int), g->stream));
-  if ((s = T.get(sizeof(uint32_t) * (nl + 1), (void**)&lcnt))) return s;
-  if ((s = T.get(sizeof(uint64_t) * (nl + 1), (void**)&loff))) return s;
-  LAUNCH(T, K_LVC, launch_levels<false>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, lcnt, nullptr, nullptr, ovf, g->stream));
-  CK(cudaGetLastError());
-  uint64_t nlev = 0;
-  if ((s = scan_counts(g, T, lcnt, nl, loff, &nlev))) return s;
-  T.release(lcnt);
-  int hovf = 0;
-  CK(cudaMemcpyAsync(&hovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
-  if (hovf)
-    return fail(DEXEL_EOVERFLOW, "more than " + std::to_string(LV_D) +
-                                     " open union intervals of one level within the growth window of a column");
-  if ((s = T.get(sizeof(float2) * (nlev + 1), (void**)&lz))) return s;
-  LAUNCH(T, K_LVW, launch_levels<true>(R, ncol, P, sp, sz, L, src.zlo, src.zhi, nullptr, loff, lz, ovf, g->stream));
-  CK(cudaGetLastError());
-  if (sp) T.release(sp);
-  if (sz) T.release(sz);
+  if (P.m > 0) g->lev_ratio = (double)out->nlev / (double)P.m;
   T.release(P.mz);
   T.release(P.mk);
   T.release(P.moff);
-  out->F.loff = loff;
-  out->F.lz = lz;
+  out->F.dbase = O.dbase;
+  out->F.rel = O.rel;
+  out->F.arena = O.arena;
   out->F.R = R;
+  out->F.ndir = ndir;
   out->F.ncol = ncol;
   out->F.row0 = row0;
   out->F.nrows = nrows;
-  out->nlev = nlev;
   return DEXEL_OK;
 }
 

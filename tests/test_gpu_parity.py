@@ -240,9 +240,11 @@ def test_torch_allocator_hook(dx):
         dx.use_torch_allocator(False)
 
 
+
 def test_levels_envelope_variant_matches(dx):
-    """The alternative level-set kernel (explicit upper envelope F, DEXEL_LEVELS=envelope)
-    agrees with the oracle too: run it in a subprocess (the mode is read once per process)."""
+    """The alternative level-set kernel (explicit upper envelope of the power functions,
+    DEXEL_LEVELS=envelope) agrees with the oracle too.  Subprocess: the mode is read once
+    per process."""
     import os
     import subprocess
     import sys
@@ -250,13 +252,14 @@ def test_levels_envelope_variant_matches(dx):
 import sys; sys.path.insert(0, %r)
 import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
 from oracle.compare import compare
-for seed in range(12):
+for seed in range(16):
     rs = np.random.default_rng(77 + seed)
-    host = G.random_grid(int(rs.integers(2, 30)), int(rs.integers(2, 30)), 4, -12.0, 12.0, seed)
-    r = float(rs.choice([1.0, 2.5, 4.0, 7.0]))
+    host = G.random_grid(int(rs.integers(2, 40)), int(rs.integers(2, 30)), 4, -12.0, 12.0, seed)
+    r = float(rs.choice([1.0, 2.5, 4.0, 7.0, 16.0, 20.0, 40.0]))
     src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
-    dx.dexel_erode(src, r, dst); off, ep = dst.download(); ref = O.erode(host, r)
-    res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], res
+    for op in ("dilate", "erode"):
+        getattr(dx, "dexel_" + op)(src, r, dst); off, ep = dst.download(); ref = getattr(O, op)(host, r)
+        res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (op, r, res)
 print("OK")
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, DEXEL_LEVELS="envelope")
