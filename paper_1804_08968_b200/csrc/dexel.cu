@@ -198,9 +198,9 @@ template <bool WRITE>
 void launch_pass1(int NW, const SrcRows& src, int R, int complement, int row0, int nrows_out, uint32_t* cnt,
                   const uint64_t* moff, float2* mz, uint8_t* mk, cudaStream_t st) {
   const int64_t warps = (int64_t)nrows_out * ((src.nx + 31) / 32);
-  const unsigned blocks = (unsigned)((warps * 32 + 127) / 128);
+  const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) pass1_kernel<NWV, WRITE><<<blocks, 128, 0, st>>>(src, R, complement, row0, nrows_out, cnt, moff, mz, mk)
+#define P1(NWV) pass1_kernel<NWV, WRITE><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, cnt, moff, mz, mk)
   if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);

@@ -115,13 +115,34 @@ __device__ __forceinline__ int nearest_parent(const uint32_t (&M)[NW], int p, in
   return best <= R ? best : KNONE;
 }
 
+template <>
+__device__ __forceinline__ int nearest_parent<2>(const uint32_t (&M)[2], int p, int R) {
+  const unsigned long long m = ((unsigned long long)M[1] << 32) | M[0];
+  const unsigned long long left = m & ((2ull << p) - 1ull);          // positions <= p (p <= 62)
+  const unsigned long long right = m >> p;                            // positions >= p
+  const int dl = left ? p - (63 - __clzll(left)) : KNONE;
+  const int dr = right ? __ffsll(right) - 1 : KNONE;
+  const int d = min(dl, dr);
+  return d <= R ? d : KNONE;
+}
+
 // One warp = output columns [32*tile, 32*tile+32) of output row jr (source row j = row0 + jr).
 // NW = number of 32-bit words of the window mask (window = 32 + 2R columns).
+// The window's endpoints (S, or its complement within [z_lo, z_hi], as
+// order-preserving u32 keys) are first staged in shared memory -- one
+// contiguous copy per window column -- so the sweep loop touches no global
+// memory; windows larger than the staging area fall back to __ldg reads.
+constexpr int P1_WARPS = 4;
+constexpr int P1_STAGE = 2048;   // keys per warp (8 KB)
+
 template <int NW, bool WRITE>
-__global__ void __launch_bounds__(128) pass1_kernel(SrcRows src, int R, int complement, int row0, int nrows_out,
-                                                    uint32_t* __restrict__ cnt, const uint64_t* __restrict__ moff,
-                                                    float2* __restrict__ mz, uint8_t* __restrict__ mk) {
+__global__ void __launch_bounds__(P1_WARPS * 32) pass1_kernel(SrcRows src, int R, int complement, int row0,
+                                                               int nrows_out, uint32_t* __restrict__ cnt,
+                                                               const uint64_t* __restrict__ moff,
+                                                               float2* __restrict__ mz, uint8_t* __restrict__ mk) {
+  __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
   const int lane = threadIdx.x & 31;
+  uint32_t* stage = stage_all[threadIdx.x >> 5];
   const int ntiles = (src.nx + 31) >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= (int64_t)nrows_out * ntiles) return;  // warp-uniform
@@ -131,13 +152,42 @@ __global__ void __launch_bounds__(128) pass1_kernel(SrcRows src, int R, int comp
   const int W = 32 + 2 * R;
 
   ColCursor cur[NW];
-  uint32_t nkey[NW];
+  uint32_t sb[NW], pos[NW], end[NW], nkey[NW];
+  uint32_t total = 0;
 #pragma unroll
   for (int q = 0; q < NW; ++q) {
     const int w = lane + 32 * q;
     if (w < W) col_open(src, i0 - R + w, j, complement, cur[q]);
     else { cur[q].base = 0; cur[q].n = 0; cur[q].v = 0; cur[q].vend = 0; }
-    nkey[q] = cur[q].v < cur[q].vend ? fkey(col_value(src, cur[q], cur[q].v, complement)) : KEY_NONE;
+    const uint32_t nv = cur[q].vend - cur[q].v;
+    uint32_t incl = nv;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    sb[q] = total + incl - nv;
+    total += __shfl_sync(FULL, incl, 31);
+  }
+  const bool staged = total <= (uint32_t)P1_STAGE;
+  if (staged) {
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      const uint32_t nv = cur[q].vend - cur[q].v;
+      for (uint32_t t = 0; t < nv; ++t) stage[sb[q] + t] = fkey(col_value(src, cur[q], cur[q].v + t, complement));
+      pos[q] = sb[q];
+      end[q] = sb[q] + nv;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < NW; ++q) nkey[q] = pos[q] < end[q] ? stage[pos[q]] : KEY_NONE;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      pos[q] = cur[q].v;
+      end[q] = cur[q].vend;
+      nkey[q] = pos[q] < end[q] ? fkey(col_value(src, cur[q], pos[q], complement)) : KEY_NONE;
+    }
   }
 
   const int i = i0 + lane;
@@ -159,10 +209,12 @@ __global__ void __launch_bounds__(128) pass1_kernel(SrcRows src, int R, int comp
 #pragma unroll
     for (int q = 0; q < NW; ++q) {
       if (nkey[q] == zk) {
-        const bool is_start = (cur[q].v & 1u) == 0u;
-        act = is_start ? (act | (1u << q)) : (act & ~(1u << q));
-        cur[q].v++;
-        nkey[q] = cur[q].v < cur[q].vend ? fkey(col_value(src, cur[q], cur[q].v, complement)) : KEY_NONE;
+        // virtual index parity: even = interval start (cur.v is even)
+        const uint32_t rel = pos[q] - (staged ? sb[q] : 0u) + (staged ? cur[q].v : 0u);
+        act = (rel & 1u) == 0u ? (act | (1u << q)) : (act & ~(1u << q));
+        ++pos[q];
+        nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(col_value(src, cur[q], pos[q], complement)))
+                                  : KEY_NONE;
       }
     }
     uint32_t M[NW];

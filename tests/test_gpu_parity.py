@@ -265,3 +265,30 @@ print("OK")
     env = dict(os.environ, DEXEL_LEVELS="envelope")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("op", ["dilate", "erode", "shell"])
+def test_many_intervals_fallback(dx, op):
+    """Columns whose result holds more intervals than the shared-memory accumulator
+    (ACC_S = 32) take the local-memory pass-2 kernel; results still match the oracle."""
+    col = [(float(t) * 0.5 - 40.0, float(t) * 0.5 - 39.8) for t in range(120)]   # 120 thin layers
+    cols = [col if (i + j) % 3 == 0 else [] for j in range(4) for i in range(5)]
+    host = _grid(5, 4, cols, -41.0, 41.0)
+    for r in (0.05, 1.2):
+        off, ep, _ = run_gpu(dx, host, op, r)
+        check(off, ep, run_oracle(host, op, r), what=f"many-intervals {op} r={r}")
+
+
+def test_pass1_bitwise_unstaged_windows(dx):
+    """Windows with more endpoints than the shared-memory staging area (2048 keys per warp)
+    take the global-memory path of the pass-1 sweep; pieces stay bitwise equal."""
+    col = [(float(t) * 0.5 - 40.0, float(t) * 0.5 - 39.8) for t in range(120)]
+    cols = [col if (i * 7 + j) % 3 else col[::2] for j in range(3) for i in range(40)]
+    host = _grid(40, 3, cols, -41.0, 41.0)
+    src = dx.Grid.from_host(host)
+    for r in (1.0, 6.0):
+        for comp in (False, True):
+            off, z, k = dx.dexel_pass1(src, r, comp)
+            ref = O.pass1(host, r, complement=comp)
+            assert np.array_equal(off, ref.off) and np.array_equal(z.astype(np.float64), ref.z) \
+                and np.array_equal(k, ref.k)
