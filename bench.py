@@ -174,22 +174,27 @@ def run_reference(a, rank, world):
 
 # ------------------------------------------------------------------ algorithmic bytes
 def algorithmic_bytes(kind, st, ncol, R_list, nfam):
-    """unique HBM bytes the method must move per kernel kind (all launches of one op), DESIGN.md 'Roofline'."""
+    """Unique HBM bytes the method must move, per kernel kind, summed over the op's
+    launches of that kind: every array the kernel must read
+    or write, counted once -- re-reads (the COUNT/WRITE recomputation, halo rows,
+    L1/L2 re-use) are not algorithmic.
+      input CSR     8 B/column offset + 8 B/interval        (n_in)
+      S_Mid pieces  8 B z-pair + 1 B kappa per piece       (n_mid), 8 B/column offset
+      level lists   8 B/interval (n_lev) + per column 8 B base + 4 B per (dir, level) start
+      output CSR    8 B/column offset + 8 B/interval        (n_out)"""
     n_in, m, nl, n_out = st["n_in"], st["n_mid"], st["n_lev"], st["n_out"]
     off = 8 * (ncol + 1)
-    lev_off = sum(8 * ((R + 1) * ncol + 1) for R in R_list)
-    if kind == "pass1_write":   # read S CSR, write pieces (8 B z-pair + 1 B kappa) + read piece offsets
-        return nfam * (off + 8 * n_in + off) + 9 * m
-    if kind == "pass1_count":   # read S CSR, write u32 counts
+    lev_dir = sum((8 + 4 * (2 * (R + 1) + 1)) * ncol for R in R_list)
+    if kind == "pass1_count":    # read the input CSR, write u32 counts
         return nfam * (off + 8 * n_in + 4 * ncol)
-    if kind == "levels_write":  # read pieces + offsets, write level intervals + read level offsets
-        return nfam * off + 9 * m + 8 * nl + lev_off
-    if kind == "levels_count":
-        return nfam * off + 9 * m + sum(4 * (R + 1) * ncol for R in R_list)
-    if kind == "pass2_write":   # read level intervals + offsets once, write output + read output offsets
-        return 8 * nl + lev_off + 8 * n_out + off
-    if kind == "pass2_count":
-        return 8 * nl + lev_off + 4 * ncol
+    if kind == "pass1_write":    # read the input CSR and piece offsets, write pieces
+        return nfam * (off + 8 * n_in + off) + 9 * m
+    if kind == "levels_write":   # read pieces (+ offsets), write level lists + directory
+        return nfam * off + 9 * m + 8 * nl + lev_dir
+    if kind == "pass2_count":    # read level lists + directory, write u32 counts
+        return 8 * nl + lev_dir + 4 * ncol
+    if kind == "pass2_write":    # read level lists + directory + output offsets, write output
+        return 8 * nl + lev_dir + off + 8 * n_out
     return 0
 
 
@@ -212,25 +217,29 @@ def run_b200(a, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist_mod
         dist = dist_mod
-        if rank == 0:
-            print(json.dumps({"error": "multi-GPU slab path is not in this build"}), flush=True)
-        sys.exit(2)
-
-    src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi, host.z_ref, 1.0, dev, stream.cuda_stream)
-    src.upload(host.off, host.ep)
-    dst = dx.Grid.like(src)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    from paper_1804_08968_b200.slabs import Slab, check_slabs
+    R = int(np.floor(a.r))
+    check_slabs(host.ny, world, R)
+    slab = Slab(host, rank, world, dev, stream.cuda_stream)
+    src, dst = slab.src, slab.dst
+    ncol_local = src.ncol   # columns this rank writes
 
     def step():
-        if a.op == "dilate":
-            dx.dexel_dilate(src, a.r, dst)
-        elif a.op == "erode":
-            dx.dexel_erode(src, a.r, dst)
-        else:
-            dx.dexel_shell(src, a.r, a.r, dst)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                slab.refresh_halos(R)          # NCCL send/recv of the R boundary rows (data-path exchange)
+        slab.op(a.op, a.r)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier(device_ids=[dev])
+        torch.cuda.synchronize()
 
     for _ in range(max(a.warmup, 3)):
         step()
-    torch.cuda.synchronize()
+    barrier()
 
     # ---- timed region: K steps, per-kernel CUDA events inside the library on the same stream
     dx.set_timing(True)
@@ -242,7 +251,7 @@ def run_b200(a, rank, world, local_rank):
     kern_ms = {k: 0.0 for k in dx.KERNEL_NAMES}
     kern_calls = {k: 0 for k in dx.KERNEL_NAMES}
     launches = 0
-    torch.cuda.synchronize()
+    barrier()
     e0.record(stream)
     for _ in range(a.steps):
         step()
@@ -252,13 +261,17 @@ def run_b200(a, rank, world, local_rank):
             kern_ms[k] += st["kernel_ms"][k]
             kern_calls[k] += st["kernel_calls"][k]
     e1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     clk = clocks.stop()
     dx.set_timing(False)
     total_ms = e0.elapsed_time(e1)
+    if dist is not None:                      # max over ranks, on the device clocks of each rank
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
     ms = total_ms / a.steps
     st = dst.stats()
-    value = ncol / (ms / 1e3)
+    value = ncol / (ms / 1e3)                 # whole-grid output columns / s (all ranks)
 
     # ---- roofline for the dominant kernel
     peak, peak_src = peaks()
@@ -266,7 +279,7 @@ def run_b200(a, rank, world, local_rank):
     nfam = 2 if a.op == "shell" else 1
     R_list = [R] * nfam
     dom = max((k for k in dx.KERNEL_NAMES if k not in ("scan", "other")), key=lambda k: kern_ms[k])
-    byts = algorithmic_bytes(dom, st, ncol, R_list, nfam)
+    byts = algorithmic_bytes(dom, st, ncol_local, R_list, nfam)
     t_dom = kern_ms[dom] / a.steps / 1e3            # s per step for that kernel kind
     achieved = byts / t_dom / 1e9 if t_dom > 0 else 0.0
     traffic = None
@@ -283,7 +296,7 @@ def run_b200(a, rank, world, local_rank):
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and world == 1:
         h_off = torch.from_numpy(host.off.view(np.int64)).pin_memory()
         h_ep = torch.from_numpy(host.ep).pin_memory()
         nout_cap = int(st["n_out"] * 1.1) + 1024
@@ -340,8 +353,13 @@ def run_b200(a, rank, world, local_rank):
         "kernel_ms_per_step": {k: v / a.steps for k, v in kern_ms.items()},
         "gpu": torch.cuda.get_device_name(dev),
     }
+    if world > 1:
+        line["config"]["slab_rows"] = [slab.y0, slab.y1]
+        line["config"]["halo_rows"] = R
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 def main():

@@ -49,10 +49,24 @@ typedef struct {
   float z_lo, z_hi;     /* domain in the local frame, finite, z_lo < z_hi */
   int32_t device;       /* CUDA ordinal */
   void* stream;         /* cudaStream_t; NULL -> library-owned stream */
-  void* nccl_comm;      /* ncclComm_t or NULL (single GPU / caller-managed halos) */
+  void* nccl_comm;      /* reserved, must be NULL: halos are exchanged by the caller (see below) */
   int32_t rank, nranks; /* slab owner; 0,1 for a single GPU */
   int32_t y0, y1;       /* owned global rows [y0,y1); 0,ny for a single GPU */
 } dexel_desc;
+
+/* Multi-GPU y-slabs ("the 2D dilations can be
+ * performed completely independently in every slice"): rank g owns rows
+ * [y0, y1) of the global grid.  Pass 1 runs along x and is row-local; pass 2
+ * runs along y and needs R = floor(r/s) rows of input beyond each slab
+ * boundary.  The caller moves them between ranks (the reference binding uses
+ * torch.distributed NCCL send/recv on device buffers):
+ *   dexel_download_rows  packs owned boundary rows as a CSR slice,
+ *   dexel_upload_halo    attaches a neighbour's rows below (side 0) or above
+ *                        (side 1) the slab.
+ * An op on a slab reads rows [y0 - halo0, y1 + halo1) and writes [y0, y1);
+ * it fails with DEXEL_EINVAL if a halo is shorter than min(R, rows to the
+ * grid edge).  Outputs of all slabs concatenated are bitwise equal to the
+ * single-GPU output (per-column results do not depend on the partition). */
 
 /* Create an empty grid (all columns empty).  *out receives the handle. */
 dexel_status dexel_create(const dexel_desc* d, dexel_grid* out);
@@ -84,6 +98,20 @@ dexel_status dexel_erode(dexel_grid src, float r, dexel_grid dst);
 /* dst := D_rout(src) \ E_rin(src) = D_rout(src) n D_rin(U \ src), per column
  * (the thick shell of PAPER.md:58-61, :847-849).  Same rules. */
 dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst);
+
+/* Attach halo rows (multi-GPU slabs): side 0 = the nrows global rows directly
+ * below y0, side 1 = the nrows rows directly above y1 (row-major CSR of
+ * nrows*nx columns, same conventions and validation as dexel_upload).  nrows
+ * = 0 removes the halo.  Synchronises the stream. */
+dexel_status dexel_upload_halo(dexel_grid g, int side, const uint64_t* offsets, const float* endpoints,
+                               int nrows, uint64_t n_intervals, int src_on_device);
+
+/* Copy local rows [row_begin, row_begin+nrows) out as a CSR slice with offsets
+ * rebased to 0 (offsets: nrows*nx+1 entries).  *n_intervals always receives
+ * the slice size; offsets == NULL only queries it; capacity < size ->
+ * DEXEL_EOVERFLOW.  Synchronises the stream. */
+dexel_status dexel_download_rows(dexel_grid g, int row_begin, int nrows, uint64_t* offsets, float* endpoints,
+                                 uint64_t capacity_intervals, uint64_t* n_intervals, int dst_on_device);
 
 /* Number of intervals currently held (local slab). */
 dexel_status dexel_size(dexel_grid g, uint64_t* n_intervals);

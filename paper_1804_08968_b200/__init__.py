@@ -25,7 +25,8 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
-           "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing"]
+           "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
+           "dexel_download_rows"]
 
 
 class DexelError(RuntimeError):
@@ -82,6 +83,8 @@ def lib():
             "dexel_set_allocator": ([ALLOC_FN, FREE_FN, vp], ctypes.c_int),
             "dexel_last_stats": ([vp, ctypes.POINTER(dexel_stats)], ctypes.c_int),
             "dexel_set_timing": ([ctypes.c_int], ctypes.c_int),
+            "dexel_upload_halo": ([vp, ctypes.c_int, vp, vp, ctypes.c_int, u64, ctypes.c_int], ctypes.c_int),
+            "dexel_download_rows": ([vp, ctypes.c_int, ctypes.c_int, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -190,6 +193,38 @@ class Grid:
         ep = np.empty(max(2 * n, 2), dtype=np.float32)
         _check(lib().dexel_download(self.h, off.ctypes.data, ep.ctypes.data, n, 0))
         return off, ep[:2 * n]
+
+    def upload_halo(self, side: int, off, ep, nrows: int):
+        """attach nrows halo rows below (side 0) or above (side 1) the slab (numpy or CUDA tensors)."""
+        if nrows == 0:
+            _check(lib().dexel_upload_halo(self.h, side, None, None, 0, 0, 0))
+            return
+        if isinstance(off, np.ndarray):
+            off = np.ascontiguousarray(off, dtype=np.uint64)
+            ep = np.ascontiguousarray(ep, dtype=np.float32)
+        n = int(off[-1]) if isinstance(off, np.ndarray) else int(ep.numel()) // 2
+        _check(lib().dexel_upload_halo(self.h, side, _ptr(off), _ptr(ep) if n else None, nrows, n,
+                                       1 if _is_dev(off) else 0))
+
+    def download_rows(self, row_begin: int, nrows: int, device: bool = False):
+        """local rows [row_begin, row_begin+nrows) as a CSR slice (offsets rebased to 0)."""
+        L = lib()
+        n = ctypes.c_uint64()
+        _check(L.dexel_download_rows(self.h, row_begin, nrows, None, None, 0, ctypes.byref(n), 0))
+        nc = nrows * self.desc.nx
+        if device:
+            import torch
+            dev = torch.device("cuda", self.desc.device)
+            off = torch.empty(nc + 1, dtype=torch.int64, device=dev)
+            ep = torch.empty(max(2 * n.value, 2), dtype=torch.float32, device=dev)
+            _check(L.dexel_download_rows(self.h, row_begin, nrows, off.data_ptr(), ep.data_ptr(), n.value,
+                                         ctypes.byref(n), 1))
+            return off, ep[:2 * n.value]
+        off = np.empty(nc + 1, dtype=np.uint64)
+        ep = np.empty(max(2 * n.value, 2), dtype=np.float32)
+        _check(L.dexel_download_rows(self.h, row_begin, nrows, off.ctypes.data, ep.ctypes.data, n.value,
+                                     ctypes.byref(n), 0))
+        return off, ep[:2 * n.value]
 
     def stats(self) -> dict:
         s = dexel_stats()

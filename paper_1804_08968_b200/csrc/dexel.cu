@@ -58,9 +58,19 @@ struct dexel_grid_s {
   uint64_t n = 0;
   dexel_stats stats{};
   double lev_ratio = 0.0;   // n_lev / n_mid of the last op (arena sizing hint)
+  // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
+  Buf hoff[2], hep[2];
+  int hrows[2] = {0, 0};
+  uint64_t hn[2] = {0, 0};
 };
 
 namespace {
+
+// dst[t] = src[t] - src[0] + add, t in [0, n]
+__global__ void rebase_offsets(const uint64_t* __restrict__ src, uint64_t n, uint64_t add, uint64_t* __restrict__ dst) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= n) dst[t] = src[t] - src[0] + add;
+}
 
 dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
   b.bytes = bytes;
@@ -441,7 +451,6 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   dexel_status s;
   if ((s = check_radius(r_a, src->d.spacing, &Ra))) return s;
   if ((s = check_radius(r_b, src->d.spacing, &Rb))) return s;
-  if (src->d.nranks > 1) return fail(DEXEL_EINVAL, "multi-rank slabs: use the slab API (not in this build)");
   CK(cudaSetDevice(src->d.device));
   cudaStream_t st = src->stream;
   if (dst->stream != st) {  // order dst's stream after src's
@@ -453,18 +462,55 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   }
   dexel_stats stats{};
   Temps T(src, &stats);
-  SrcRows rows{(const uint64_t*)src->off.p, (const float*)src->ep.p, src->d.nx, src->nrows, src->d.z_lo,
-               src->d.z_hi};
+  // halo rows (y-slabs): the op reads rows [y0 - hlo, y1 + hhi) and writes [y0, y1)
+  const int Rmax = Ra > Rb ? Ra : Rb;
+  const int need_lo = src->d.y0 < Rmax ? src->d.y0 : Rmax;
+  const int need_hi = src->d.ny - src->d.y1 < Rmax ? src->d.ny - src->d.y1 : Rmax;
+  if (src->hrows[0] < need_lo || src->hrows[1] < need_hi)
+    return fail(DEXEL_EINVAL, "slab halo too small: need " + std::to_string(need_lo) + " rows below and " +
+                                  std::to_string(need_hi) + " above (dexel_upload_halo)");
+  const int hlo = src->hrows[0], hhi = src->hrows[1];
+  const int nrows_ext = hlo + src->nrows + hhi;
+  const uint64_t* ext_off = (const uint64_t*)src->off.p;
+  const float* ext_ep = (const float*)src->ep.p;
+  if (hlo || hhi) {
+    const int64_t nx = src->d.nx;
+    const int64_t ncol_ext = (int64_t)nrows_ext * nx;
+    const uint64_t next = src->hn[0] + src->n + src->hn[1];
+    uint64_t* eo = nullptr;
+    float2* ee = nullptr;
+    if ((s = T.get(sizeof(uint64_t) * (ncol_ext + 1), (void**)&eo))) return s;
+    if ((s = T.get(sizeof(float2) * (next + 1), (void**)&ee))) return s;
+    const Buf* parts_off[3] = {&src->hoff[0], &src->off, &src->hoff[1]};
+    const Buf* parts_ep[3] = {&src->hep[0], &src->ep, &src->hep[1]};
+    const int64_t part_cols[3] = {(int64_t)hlo * nx, src->ncol, (int64_t)hhi * nx};
+    const uint64_t part_n[3] = {src->hn[0], src->n, src->hn[1]};
+    int64_t cbase = 0;
+    uint64_t ebase = 0;
+    for (int q = 0; q < 3; ++q) {
+      if (part_cols[q] == 0) continue;
+      rebase_offsets<<<(unsigned)((part_cols[q] + 256) / 256), 256, 0, st>>>(
+          (const uint64_t*)parts_off[q]->p, (uint64_t)part_cols[q], ebase, eo + cbase);
+      if (part_n[q]) CK(cudaMemcpyAsync(ee + ebase, parts_ep[q]->p, sizeof(float2) * part_n[q],
+                                        cudaMemcpyDeviceToDevice, st));
+      cbase += part_cols[q];
+      ebase += part_n[q];
+    }
+    CK(cudaGetLastError());
+    ext_off = eo;
+    ext_ep = (const float*)ee;
+  }
+  SrcRows rows{ext_off, ext_ep, src->d.nx, nrows_ext, src->d.z_lo, src->d.z_hi};
   stats.n_in = src->n;
   Family FA, FB;
   // family A: dilate S (dilate, shell r_out) or C (erode)
-  if ((s = run_family(src, T, rows, r_a, op == OP_ERODE ? 1 : 0, 0, src->nrows, &FA, &stats.n_mid))) {
+  if ((s = run_family(src, T, rows, r_a, op == OP_ERODE ? 1 : 0, 0, nrows_ext, &FA, &stats.n_mid))) {
     set_empty(dst);
     return s;
   }
   stats.n_lev = FA.nlev;
   if (op == OP_SHELL) {
-    if ((s = run_family(src, T, rows, r_b, 1, 0, src->nrows, &FB, &stats.n_mid))) {
+    if ((s = run_family(src, T, rows, r_b, 1, 0, nrows_ext, &FB, &stats.n_mid))) {
       set_empty(dst);
       return s;
     }
@@ -479,7 +525,7 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
   if ((s = T.get(sizeof(int) * 4, (void**)&ovf))) return s;
   CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-  LAUNCH(T, K_P2C, launch_pass2<false>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, ocnt,
+  LAUNCH(T, K_P2C, launch_pass2<false>(op, FA.F, FB.F, src->d.nx, hlo, src->nrows, src->d.z_lo, src->d.z_hi, ocnt,
                                        nullptr, nullptr, ovf, st));
   CK(cudaGetLastError());
   uint64_t nout = 0;
@@ -495,8 +541,8 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   }
   dfree(dst, dst->ep);
   if ((s = dalloc(dst, dst->ep, sizeof(float2) * (nout + 1)))) return s;
-  LAUNCH(T, K_P2W, launch_pass2<true>(op, FA.F, FB.F, src->d.nx, 0, src->nrows, src->d.z_lo, src->d.z_hi, nullptr,
-                                      (const uint64_t*)dst->off.p, (float2*)dst->ep.p, ovf, st));
+  LAUNCH(T, K_P2W, launch_pass2<true>(op, FA.F, FB.F, src->d.nx, hlo, src->nrows, src->d.z_lo, src->d.z_hi,
+                                      nullptr, (const uint64_t*)dst->off.p, (float2*)dst->ep.p, ovf, st));
   CK(cudaGetLastError());
   dst->n = nout;
   stats.n_out = nout;
@@ -575,12 +621,14 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
   return DEXEL_OK;
 }
 
-dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev) {
-  g_err.clear();
-  if (!g || !offsets || (n > 0 && !endpoints)) return fail(DEXEL_EINVAL, "NULL argument");
+}  // extern "C"
+
+namespace {
+// copy + validate a CSR of ncol columns into fresh buffers (grid unchanged on error)
+dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoints, int64_t ncol, uint64_t n,
+                      int on_dev, Buf* off_out, Buf* ep_out) {
+  if (!offsets || (n > 0 && !endpoints)) return fail(DEXEL_EINVAL, "NULL argument");
   CK(cudaSetDevice(g->d.device));
-  const int64_t ncol = g->ncol;
-  // host-side checks of the offsets frame
   uint64_t first = 0, last = 0;
   if (on_dev) {
     CK(cudaMemcpyAsync(&first, offsets, 8, cudaMemcpyDeviceToHost, g->stream));
@@ -625,11 +673,80 @@ dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* en
                                   ", local row " + std::to_string(c / g->d.nx) +
                                   "): intervals must be finite, strictly increasing and inside [z_lo, z_hi]");
   }
+  *off_out = off;
+  *ep_out = ep;
+  return DEXEL_OK;
+}
+}  // namespace
+
+extern "C" {
+
+dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev) {
+  g_err.clear();
+  if (!g) return fail(DEXEL_EINVAL, "NULL handle");
+  Buf off, ep;
+  dexel_status s = load_csr(g, offsets, endpoints, g->ncol, n, on_dev, &off, &ep);
+  if (s) return s;
   dfree(g, g->off);
   dfree(g, g->ep);
   g->off = off;
   g->ep = ep;
   g->n = n;
+  return DEXEL_OK;
+}
+
+dexel_status dexel_upload_halo(dexel_grid g, int side, const uint64_t* offsets, const float* endpoints, int nrows,
+                               uint64_t n, int on_dev) {
+  g_err.clear();
+  if (!g || (side != 0 && side != 1) || nrows < 0) return fail(DEXEL_EINVAL, "bad halo arguments");
+  const int avail = side == 0 ? g->d.y0 : g->d.ny - g->d.y1;
+  if (nrows > avail) return fail(DEXEL_EINVAL, "halo extends past the grid");
+  dfree(g, g->hoff[side]);
+  dfree(g, g->hep[side]);
+  g->hrows[side] = 0;
+  g->hn[side] = 0;
+  if (nrows == 0) return DEXEL_OK;
+  Buf off, ep;
+  dexel_status s = load_csr(g, offsets, endpoints, (int64_t)nrows * g->d.nx, n, on_dev, &off, &ep);
+  if (s) return s;
+  g->hoff[side] = off;
+  g->hep[side] = ep;
+  g->hrows[side] = nrows;
+  g->hn[side] = n;
+  return DEXEL_OK;
+}
+
+dexel_status dexel_download_rows(dexel_grid g, int row_begin, int nrows, uint64_t* offsets, float* endpoints,
+                                 uint64_t cap, uint64_t* n_out, int on_dev) {
+  g_err.clear();
+  if (!g || !n_out || row_begin < 0 || nrows < 0 || row_begin + nrows > g->nrows)
+    return fail(DEXEL_EINVAL, "bad row range");
+  CK(cudaSetDevice(g->d.device));
+  const int64_t c0 = (int64_t)row_begin * g->d.nx, nc = (int64_t)nrows * g->d.nx;
+  uint64_t ab[2] = {0, 0};
+  CK(cudaMemcpyAsync(&ab[0], (uint64_t*)g->off.p + c0, 8, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaMemcpyAsync(&ab[1], (uint64_t*)g->off.p + c0 + nc, 8, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  const uint64_t n = ab[1] - ab[0];
+  *n_out = n;
+  if (!offsets) return DEXEL_OK;   // size query
+  if (cap < n) return fail(DEXEL_EOVERFLOW, "capacity < intervals in the rows");
+  if (!offsets || (n && !endpoints)) return fail(DEXEL_EINVAL, "NULL output buffer");
+  Temps T(g);
+  uint64_t* tmp = nullptr;
+  dexel_status s;
+  if (on_dev) {
+    tmp = offsets;
+  } else if ((s = T.get(sizeof(uint64_t) * (nc + 1), (void**)&tmp))) {
+    return s;
+  }
+  rebase_offsets<<<(unsigned)((nc + 256) / 256), 256, 0, g->stream>>>((const uint64_t*)g->off.p + c0, (uint64_t)nc,
+                                                                       0, tmp);
+  CK(cudaGetLastError());
+  const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (!on_dev) CK(cudaMemcpyAsync(offsets, tmp, sizeof(uint64_t) * (nc + 1), k, g->stream));
+  if (n) CK(cudaMemcpyAsync(endpoints, (const float2*)g->ep.p + ab[0], sizeof(float2) * n, k, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
   return DEXEL_OK;
 }
 
@@ -702,6 +819,10 @@ void dexel_destroy(dexel_grid g) {
   cudaSetDevice(g->d.device);
   dfree(g, g->off);
   dfree(g, g->ep);
+  for (int q = 0; q < 2; ++q) {
+    dfree(g, g->hoff[q]);
+    dfree(g, g->hep[q]);
+  }
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
