@@ -177,24 +177,24 @@ def algorithmic_bytes(kind, st, ncol, R_list, nfam):
     """Unique HBM bytes the method must move, per kernel kind, summed over the op's
     launches of that kind: every array the kernel must read
     or write, counted once -- re-reads (the COUNT/WRITE recomputation, halo rows,
-    L1/L2 re-use) are not algorithmic.
-      input CSR     8 B/column offset + 8 B/interval        (n_in)
-      S_Mid pieces  8 B z-pair + 1 B kappa per piece       (n_mid), 8 B/column offset
-      level lists   8 B/interval (n_lev) + per column 8 B base + 4 B per (dir, level) start
-      output CSR    8 B/column offset + 8 B/interval        (n_out)"""
+    the two output rows that read each level list, L1/L2 re-use) are not algorithmic.
+      input CSR     8 B/column offset + 8 B/interval               (n_in)
+      S_Mid pieces  8 B z-pair + 1 B kappa per piece, 8 B/column    (n_mid)
+      level sets    8 B/interval (n_lev) + 1 B count per (column, level)
+      output        8 B/interval (n_out) + 4 B count per column (staging), then CSR"""
     n_in, m, nl, n_out = st["n_in"], st["n_mid"], st["n_lev"], st["n_out"]
     off = 8 * (ncol + 1)
-    lev_dir = sum((8 + 4 * (2 * (R + 1) + 1)) * ncol for R in R_list)
+    lev_cnt = sum((R + 1) * ncol for R in R_list)
     if kind == "pass1_count":    # read the input CSR, write u32 counts
         return nfam * (off + 8 * n_in + 4 * ncol)
     if kind == "pass1_write":    # read the input CSR and piece offsets, write pieces
         return nfam * (off + 8 * n_in + off) + 9 * m
-    if kind == "levels_write":   # read pieces (+ offsets), write level lists + directory
-        return nfam * off + 9 * m + 8 * nl + lev_dir
-    if kind == "pass2_count":    # read level lists + directory, write u32 counts
-        return 8 * nl + lev_dir + 4 * ncol
-    if kind == "pass2_write":    # read level lists + directory + output offsets, write output
-        return 8 * nl + lev_dir + off + 8 * n_out
+    if kind == "levels":         # read pieces (+ offsets), write level slots + counts
+        return nfam * off + 9 * m + 8 * nl + lev_cnt
+    if kind == "pass2":          # read level slots + counts, write staged output + counts
+        return 8 * nl + lev_cnt + 8 * n_out + 4 * ncol
+    if kind == "compact":        # read staged output + counts + offsets, write the output CSR
+        return 8 * n_out + 4 * ncol + off + 8 * n_out
     return 0
 
 

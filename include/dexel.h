@@ -149,18 +149,21 @@ typedef void (*dexel_free_fn)(void* ptr, size_t bytes, int device, void* stream,
 dexel_status dexel_set_allocator(dexel_alloc_fn alloc, dexel_free_fn free_, void* ctx);
 
 /* Per-op statistics of the last op on handle g (for measurement):
- * n_in, n_mid (pass-1 pieces), n_lev (level-set intervals), n_out; the
+ * n_in, n_mid (pass-1 pieces), n_lev (level-set intervals L_k), n_out; the
  * number of kernels the op launched; and, when timing is on
  * (dexel_set_timing(1)), the summed device time and launch count of each
  * kernel kind, measured with CUDA events on the handle's stream:
- *   0 pass1 count, 1 pass1 write, 2 levels count, 3 levels write,
- *   4 pass2 count, 5 pass2 write, 6 scan, 7 other. */
+ *   0 pass1 count, 1 pass1 write, 2 levels (envelope), 3 pass2,
+ *   4 compaction, 5 scan, 6 other, 7 reserved. */
 #define DEXEL_NKERNELS 8
 typedef struct {
   uint64_t n_in, n_mid, n_lev, n_out;
   uint32_t launches;
   uint32_t kernel_calls[DEXEL_NKERNELS];
   float kernel_ms[DEXEL_NKERNELS];
+  /* capacities the op ran with: level slots per list,
+   * pass-2 accumulator, number of row bands */
+  uint32_t lev_cap, p2_acc, bands;
 } dexel_stats;
 dexel_status dexel_last_stats(dexel_grid g, dexel_stats* out);
 

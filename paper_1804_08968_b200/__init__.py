@@ -44,14 +44,14 @@ class dexel_desc(ctypes.Structure):
 
 
 NKERNELS = 8
-KERNEL_NAMES = ["pass1_count", "pass1_write", "levels_count", "levels_write", "pass2_count", "pass2_write",
-                "scan", "other"]
+KERNEL_NAMES = ["pass1_count", "pass1_write", "levels", "pass2", "compact", "scan", "other", "reserved"]
 
 
 class dexel_stats(ctypes.Structure):
     _fields_ = [("n_in", ctypes.c_uint64), ("n_mid", ctypes.c_uint64), ("n_lev", ctypes.c_uint64),
                 ("n_out", ctypes.c_uint64), ("launches", ctypes.c_uint32),
-                ("kernel_calls", ctypes.c_uint32 * NKERNELS), ("kernel_ms", ctypes.c_float * NKERNELS)]
+                ("kernel_calls", ctypes.c_uint32 * NKERNELS), ("kernel_ms", ctypes.c_float * NKERNELS),
+                ("lev_cap", ctypes.c_uint32), ("p2_acc", ctypes.c_uint32), ("bands", ctypes.c_uint32)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
@@ -231,7 +231,8 @@ class Grid:
         _check(lib().dexel_last_stats(self.h, ctypes.byref(s)))
         return dict(n_in=s.n_in, n_mid=s.n_mid, n_lev=s.n_lev, n_out=s.n_out, launches=s.launches,
                     kernel_calls=dict(zip(KERNEL_NAMES, list(s.kernel_calls))),
-                    kernel_ms=dict(zip(KERNEL_NAMES, list(s.kernel_ms))))
+                    kernel_ms=dict(zip(KERNEL_NAMES, list(s.kernel_ms))),
+                    capacities=dict(lev_cap=s.lev_cap, p2_acc=s.p2_acc, bands=s.bands))
 
     def sync(self):
         _check(lib().dexel_sync(self.h))

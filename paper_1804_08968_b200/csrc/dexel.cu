@@ -3,10 +3,15 @@
 //
 // Op pipeline (one "family" per dilation; erode and shell dilate the
 // complement, which pass 1 reads on the fly):
-//   pass1 COUNT -> scan -> pass1 WRITE          S_In -> S_Mid (pieces lo,hi,kappa)
-//   levels COUNT -> scan -> levels WRITE        S_Mid -> {L_k}, k = 0..R
-//   pass2 COUNT -> scan -> pass2 WRITE          {L_k} -> S_Out (+ epilogue)
-// Each scan ends with one 8-byte device->host read of the total (allocation size).
+//   pass1 COUNT -> scan -> pass1 WRITE     S_In -> S_Mid (pieces lo,hi,kappa), CSR
+//   levels (envelope)                      S_Mid -> level slots L_k, k = 0..R
+//   pass2 (+ epilogue) -> scan -> compact  {L_k} -> S_Out (output CSR)
+// Host synchronisations per family: the pass-1 total (allocation size) and the
+// level kernel's capacity flags; per op: the pass-2 flags and the output total.
+// A capacity overflow (level list > cap, envelope deque > D, pass-2 union >
+// acc) reruns that stage with a larger capacity; the sizes are kept as hints
+// on the handle for later ops.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +21,8 @@
 
 #include "dexel.h"
 #include "kernels.cuh"
+#include "levels.cuh"
+#include "pass2.cuh"
 #include "scan.cuh"
 
 using namespace dexel;
@@ -57,7 +64,8 @@ struct dexel_grid_s {
   Buf off, ep;
   uint64_t n = 0;
   dexel_stats stats{};
-  double lev_ratio = 0.0;   // n_lev / n_mid of the last op (arena sizing hint)
+  // capacity hints carried between ops (grown on overflow)
+  int lev_cap = 0, p2_acc = 0;
   // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
   Buf hoff[2], hep[2];
   int hrows[2] = {0, 0};
@@ -99,7 +107,7 @@ void dfree(dexel_grid g, Buf& b) {
 }
 
 // per-op kernel accounting: launch counts always, CUDA-event device times when g_timing
-enum { K_P1C = 0, K_P1W = 1, K_LVC = 2, K_LVW = 3, K_P2C = 4, K_P2W = 5, K_SCAN = 6, K_OTHER = 7 };
+enum { K_P1C = 0, K_P1W = 1, K_LEV = 2, K_P2 = 3, K_COMPACT = 4, K_SCAN = 5, K_OTHER = 6 };
 struct Prof {
   cudaStream_t st = nullptr;
   dexel_stats* s = nullptr;
@@ -246,190 +254,152 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
 }
 
 // ---------------------------------------------------------------- levels
-struct Family {
-  LevelFamily F;
-  uint64_t nlev = 0;
-};
-
-dexel_status make_tables(dexel_grid g, Temps& T, float r, int R, LevelTables* L, EnvTables* E) {
+// h(kappa,k) = sqrt(r^2 - (kappa^2 + k^2) s^2) computed in fp64 on the host and rounded once
+// to fp32 (readings R10, R20), -1 where kappa^2 + k^2 > (r/s)^2: the device never
+// evaluates a square root of a weight, and which (kappa, k) contribute is decided exactly.
+dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out) {
   const double s = g->d.spacing;
   const int n1 = R + 1;
   std::vector<float> h((size_t)n1 * n1);
-  std::vector<double> W(n1), Tk(n1);
   const double rr = (double)r * (double)r;
-  for (int a = 0; a < n1; ++a) {
-    W[a] = rr - (double)a * a * s * s;
-    Tk[a] = (double)a * a * s * s;
-  }
   for (int a = 0; a < n1; ++a)
     for (int k = 0; k < n1; ++k) {
-      // W(kappa) - T(k) in fp64, rounded once to fp32; valid iff T(k) <= W(kappa)
-      const double w = W[a] - Tk[k];
+      const double w = rr - ((double)a * a + (double)k * k) * s * s;   // exact for fp32 r, small integers
       h[(size_t)a * n1 + k] = w >= 0.0 ? (float)std::sqrt(w) : -1.0f;
     }
-  char* buf = nullptr;
-  const size_t hb = sizeof(float) * h.size(), db = sizeof(double) * n1;
   dexel_status st;
-  if ((st = T.get(hb + 2 * db + 64, (void**)&buf))) return st;
-  double* dW = (double*)buf;
-  double* dT = dW + n1;
-  float* dh = (float*)(dT + n1);
-  CK(cudaMemcpyAsync(dW, W.data(), db, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(dT, Tk.data(), db, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(dh, h.data(), hb, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaStreamSynchronize(g->stream));  // host vectors go out of scope
-  L->h = dh;
-  L->R = R;
-  E->h = dh;
-  E->W = dW;
-  E->Tk = dT;
-  E->R = R;
-  E->r = (double)r;
-  E->inv_s2 = 1.0 / (s * s);
+  if ((st = T.get(sizeof(float) * h.size() + 16, (void**)out))) return st;
+  CK(cudaMemcpyAsync(*out, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
+  CK(cudaStreamSynchronize(g->stream));  // the host vector goes out of scope
   return DEXEL_OK;
 }
 
-template <int NS>
-void launch_levels4_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
-                      const LevelOut& O, cudaStream_t st) {
-  constexpr int WARPS = Lv4Cfg<NS>::WARPS;
-  const int nl = R + 1;
-  const int G = NS == 1 ? 32 / nl : 1;
-  const int h_in_smem = sizeof(float) * nl * nl <= 64 * 1024 ? 1 : 0;
-  const size_t smem = sizeof(float2) * WARPS * 2 * NS * STG_C * 32 + (h_in_smem ? sizeof(float) * nl * nl : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(levels4_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  const int64_t per_block = (int64_t)WARPS * G;
-  const unsigned blocks = (unsigned)((ncol + per_block - 1) / per_block);
-  if (blocks == 0) return;
-  levels4_kernel<NS><<<blocks, WARPS * 32, smem, st>>>(ncol, P.moff, P.mz, P.mk, L, h_in_smem, zlo, zhi, O);
-}
-
-template <int LMAX>
-void launch_levels5_t(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
-                      const LevelOut& O, cudaStream_t st) {
-  (void)R;
-  const unsigned blocks = (unsigned)((ncol + 127) / 128);
-  if (blocks == 0) return;
-  levels5_kernel<LMAX><<<blocks, 128, 0, st>>>(ncol, P.moff, P.mz, P.mk, L, zlo, zhi, O);
-}
-
-void launch_levels(int R, int64_t ncol, const Pieces& P, const LevelTables& L, float zlo, float zhi,
-                   const LevelOut& O, cudaStream_t st) {
-  const int nl = R + 1;
-  // R < 17: one thread per column, 2(R+1) running unions in registers (levels5);
-  // larger R: one warp per column, lanes = levels (levels4)
-  if (nl <= 2) launch_levels5_t<2>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 3) launch_levels5_t<3>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 5) launch_levels5_t<5>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 9) launch_levels5_t<9>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 17) launch_levels5_t<17>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 32) launch_levels4_t<1>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 64) launch_levels4_t<2>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 96) launch_levels4_t<3>(R, ncol, P, L, zlo, zhi, O, st);
-  else if (nl <= 128) launch_levels4_t<4>(R, ncol, P, L, zlo, zhi, O, st);
-  else launch_levels4_t<8>(R, ncol, P, L, zlo, zhi, O, st);
-}
-
-// level-set kernel: 1 = per-level running unions (levels5 for R < 17, levels4 above;
-// default), 0 = power-diagram envelope (levels6; DEXEL_LEVELS=envelope, cross-checked
-// in tests)
-int levels_mode() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("DEXEL_LEVELS");
-    v = (e && std::strcmp(e, "envelope") == 0) ? 0 : 1;
-  }
-  return v;
-}
-
-// one dilation family: rows [row0, row0+nrows) of src (S or its complement) at radius r
-dexel_status run_family(dexel_grid g, Temps& T, const SrcRows& src, float r, int complement, int row0, int nrows,
-                        Family* out, uint64_t* n_mid) {
-  int R;
+// level slots of one family for level rows [lr0, lr0 + lrn) (extended-row numbering):
+// pass 1 on those rows, then the level-set kernel; the pieces are freed on return.
+// A level list longer than the slot capacity reruns the level kernel with a larger cap.
+dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, int complement,
+                        int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev) {
   dexel_status s;
-  if ((s = check_radius(r, g->d.spacing, &R))) return s;
   Pieces P;
-  if ((s = run_pass1(g, T, src, R, complement, row0, nrows, &P))) return s;
+  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P))) return s;
   *n_mid += P.m;
-  LevelTables L;
-  EnvTables E;
-  if ((s = make_tables(g, T, r, R, &L, &E))) return s;
-  const int64_t ncol = (int64_t)nrows * src.nx;
-  const int ndir = levels_mode() == 0 ? 1 : 2;
-  const int ntask = ndir * (R + 1);
-  LevelOut O;
-  if ((s = T.get(sizeof(uint64_t) * (ncol + 1), (void**)&O.dbase))) return s;
-  if ((s = T.get(sizeof(uint32_t) * (ncol * (ntask + 1) + 1), (void**)&O.rel))) return s;
-  if ((s = T.get(sizeof(unsigned long long) * 2, (void**)&O.counter))) return s;
-  // arena sized from the previous op's level/piece ratio (rerun with the exact size if it overflows)
-  const double ratio = g->lev_ratio > 0 ? g->lev_ratio * 1.1 : 1.5;
-  O.cap = (uint64_t)(ratio * (double)P.m) + 4096;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    if ((s = T.get(sizeof(float2) * (O.cap + 1), (void**)&O.arena))) return s;
-    CK(cudaMemsetAsync(O.counter, 0, 2 * sizeof(unsigned long long), g->stream));
-    if (ndir == 1) {
-      const size_t smem = (sizeof(float) + sizeof(uint32_t)) * (R + 1) * 128;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(levels6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
-      const unsigned blocks = (unsigned)((ncol + 127) / 128);
-      if (blocks) LAUNCH(T, K_LVW, levels6_kernel<<<blocks, 128, smem, g->stream>>>(ncol, P.moff, P.mz, P.mk, E,
-                                                                                    src.zlo, src.zhi, O));
-    } else {
-      LAUNCH(T, K_LVW, launch_levels(R, ncol, P, L, src.zlo, src.zhi, O, g->stream));
+  const int64_t ncol = (int64_t)lrn * src.nx;
+  unsigned* flags = nullptr;
+  if ((s = T.get(64, (void**)&flags))) return s;
+  unsigned long long* nlev = (unsigned long long*)(flags + 8);
+  L->R = R;
+  L->nx = src.nx;
+  L->nrows = lrn;
+  L->row0 = lr0;
+  L->cap = g->lev_cap > 0 ? g->lev_cap : 8;
+  const size_t nlist = (size_t)ncol * 2 * (R + 1);
+  if ((s = T.get(nlist + 16, (void**)&L->cnt))) return s;
+  if ((s = T.get(sizeof(int32_t) * ncol + 16, (void**)&L->ovf_idx))) return s;
+  const unsigned ovf_cap = (unsigned)std::max<int64_t>(256, ncol / 256);
+  uint32_t* ovf_list = nullptr;
+  if ((s = T.get(sizeof(uint32_t) * ovf_cap, (void**)&ovf_list))) return s;
+  // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of <= 24
+  static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17, 20, 24};
+  const int nchunk = (R + 1 + 23) / 24;
+  const int per = (R + 1 + nchunk - 1) / nchunk;
+  int lmax = 24;
+  for (int v : kChunk)
+    if (v >= per) { lmax = v; break; }
+  auto launch = [&](const LvArgs& A, int64_t nwork) {
+    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk);
+    if (nwork <= 0) return;
+    T.prof.pre(K_LEV);
+    switch (lmax) {
+#define LV(V) case V: levels_kernel<V><<<grid, LV_T, 0, g->stream>>>(A); break;
+      LV(2) LV(3) LV(4) LV(5) LV(6) LV(8) LV(10) LV(12) LV(14) LV(17) LV(20) LV(24)
+#undef LV
     }
+    T.prof.post();
+  };
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    if ((s = T.get(sizeof(float2) * nlist * L->cap + 16, (void**)&L->z))) return s;
+    CK(cudaMemsetAsync(flags, 0, 64, g->stream));
+    LvArgs A{P.moff, P.mz, P.mk, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, ovf_list, ovf_cap, nullptr, 0};
+    launch(A, ncol);
     CK(cudaGetLastError());
-    unsigned long long used2[2] = {0, 0};
-    CK(cudaMemcpyAsync(used2, O.counter, sizeof(used2), cudaMemcpyDeviceToHost, g->stream));
+    unsigned hf[2];
+    CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
-    const unsigned long long used = used2[0];
-    if (used2[1])
-      return fail(DEXEL_EOVERFLOW, ndir == 1 ? "a column's power-diagram envelope exceeds the deque capacity"
-                                             : "a column has more than 65534 intervals in one level list");
-    if (used <= O.cap) {
-      out->nlev = used;
+    if (hf[0] > (unsigned)LV_OVF_CAP)
+      return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
+    if (hf[1] <= ovf_cap) {
+      if (hf[1] > 0) {   // overflow pass: the listed columns' lists, all of them, into the arena
+        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * 2 * (R + 1) * LV_OVF_CAP + 16, (void**)&L->ovf_z))) return s;
+        LvArgs B = A;
+        B.L = *L;
+        B.list = ovf_list;
+        B.nlist = hf[1];
+        launch(B, hf[1]);
+        CK(cudaGetLastError());
+      }
+      unsigned long long hn = 0;
+      CK(cudaMemcpyAsync(&hn, nlev, sizeof(hn), cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      *n_lev += hn;
       break;
     }
-    T.release(O.arena);
-    O.cap = used;
-    if (attempt == 1) return fail(DEXEL_ECUDA, "level arena sizing did not converge");
+    // too many long lists: a larger slot capacity pays
+    T.release(L->z);
+    L->cap = std::min(LV_OVF_CAP, 2 * L->cap);
+    g->lev_cap = L->cap;
+    if (attempt == 5) return fail(DEXEL_ECUDA, "level capacity sizing did not converge");
   }
-  if (P.m > 0) g->lev_ratio = (double)out->nlev / (double)P.m;
   T.release(P.mz);
   T.release(P.mk);
   T.release(P.moff);
-  out->F.dbase = O.dbase;
-  out->F.rel = O.rel;
-  out->F.arena = O.arena;
-  out->F.R = R;
-  out->F.ndir = ndir;
-  out->F.ncol = ncol;
-  out->F.row0 = row0;
-  out->F.nrows = nrows;
+  T.release(ovf_list);
+  T.release(flags);
   return DEXEL_OK;
 }
 
-template <int OP, bool WRITE>
-void launch_pass2_t(const LevelFamily& A, const LevelFamily& B, int nx, int row0, int nrows, float zlo, float zhi,
-                    uint32_t* ocnt, const uint64_t* ooff, float2* oz, int* ovf, cudaStream_t st) {
+struct P2Out {
+  int64_t cbase, ncol;     // first output column of the band; staging stride (all output columns)
+  int acc;
+  float2* stage;
+  uint32_t* ocnt;
+  unsigned* flags;
+};
+
+template <int OP, int TT>
+void launch_pass2_t(const LevelSlots& A, const LevelSlots& B, int nx, int row0, int nrows, float zlo, float zhi,
+                    const P2Out& O, cudaStream_t st) {
+  const int acc = O.acc;
   const int64_t n = (int64_t)nrows * nx;
-  const unsigned blocks = (unsigned)((n + 127) / 128);
+  const unsigned blocks = (unsigned)((n + TT - 1) / TT);
   if (blocks == 0) return;
-  pass2_kernel<OP, WRITE><<<blocks, 128, 0, st>>>(A, B, nx, row0, nrows, zlo, zhi, ocnt, ooff, oz, ovf);
+  const size_t smem = pass2_smem_bytes(OP, acc, TT);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(pass2s_kernel<OP, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pass2s_kernel<OP, TT><<<blocks, TT, smem, st>>>(A, B, nx, row0, nrows, O.cbase, O.ncol, zlo, zhi, acc, O.stage,
+                                                  O.ocnt, O.flags);
 }
 
-template <bool WRITE>
-void launch_pass2(int op, const LevelFamily& A, const LevelFamily& B, int nx, int row0, int nrows, float zlo,
-                  float zhi, uint32_t* ocnt, const uint64_t* ooff, float2* oz, int* ovf, cudaStream_t st) {
-  if (op == OP_DILATE) launch_pass2_t<OP_DILATE, WRITE>(A, B, nx, row0, nrows, zlo, zhi, ocnt, ooff, oz, ovf, st);
-  else if (op == OP_ERODE) launch_pass2_t<OP_ERODE, WRITE>(A, B, nx, row0, nrows, zlo, zhi, ocnt, ooff, oz, ovf, st);
-  else launch_pass2_t<OP_SHELL, WRITE>(A, B, nx, row0, nrows, zlo, zhi, ocnt, ooff, oz, ovf, st);
+// block size: 128 threads while the accumulators fit, fewer for long unions
+inline int pass2_block(int op, int acc) {
+  int TT = 128;
+  while (TT > 32 && pass2_smem_bytes(op, acc, TT) > 220 * 1024) TT >>= 1;
+  return TT;
+}
+
+template <int OP>
+void launch_pass2_op(const LevelSlots& A, const LevelSlots& B, int nx, int row0, int nrows, float zlo, float zhi,
+                     const P2Out& O, cudaStream_t st) {
+  const int TT = pass2_block(OP, O.acc);
+  if (TT == 128) launch_pass2_t<OP, 128>(A, B, nx, row0, nrows, zlo, zhi, O, st);
+  else if (TT == 64) launch_pass2_t<OP, 64>(A, B, nx, row0, nrows, zlo, zhi, O, st);
+  else launch_pass2_t<OP, 32>(A, B, nx, row0, nrows, zlo, zhi, O, st);
+}
+
+void launch_pass2(int op, const LevelSlots& A, const LevelSlots& B, int nx, int row0, int nrows, float zlo,
+                  float zhi, const P2Out& O, cudaStream_t st) {
+  if (op == OP_DILATE) launch_pass2_op<OP_DILATE>(A, B, nx, row0, nrows, zlo, zhi, O, st);
+  else if (op == OP_ERODE) launch_pass2_op<OP_ERODE>(A, B, nx, row0, nrows, zlo, zhi, O, st);
+  else launch_pass2_op<OP_SHELL>(A, B, nx, row0, nrows, zlo, zhi, O, st);
 }
 
 bool same_geometry(const dexel_desc& a, const dexel_desc& b) {
@@ -502,47 +472,99 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   }
   SrcRows rows{ext_off, ext_ep, src->d.nx, nrows_ext, src->d.z_lo, src->d.z_hi};
   stats.n_in = src->n;
-  Family FA, FB;
-  // family A: dilate S (dilate, shell r_out) or C (erode)
-  if ((s = run_family(src, T, rows, r_a, op == OP_ERODE ? 1 : 0, 0, nrows_ext, &FA, &stats.n_mid))) {
-    set_empty(dst);
-    return s;
-  }
-  stats.n_lev = FA.nlev;
-  if (op == OP_SHELL) {
-    if ((s = run_family(src, T, rows, r_b, 1, 0, nrows_ext, &FB, &stats.n_mid))) {
-      set_empty(dst);
-      return s;
-    }
-    stats.n_lev += FB.nlev;
-  } else {
-    FB = FA;
-  }
-  // pass 2
+  // h(kappa, k) tables, one per family radius
+  float* htab_a = nullptr;
+  float* htab_b = nullptr;
+  if ((s = make_htab(src, T, r_a, Ra, &htab_a))) return s;
+  if (op == OP_SHELL && (s = make_htab(src, T, r_b, Rb, &htab_b))) return s;
+  // ---- row bands: level slots of (band + R-row halo) rows, then pass 2 of the band
   const int64_t ncol = src->ncol;
+  const int nx = src->d.nx;
+  const int nfam = op == OP_SHELL ? 2 : 1;
+  int lcap = src->lev_cap > 0 ? src->lev_cap : 8;
+  size_t row_bytes = 0;   // level-slot bytes per level row, all families
+  for (int f = 0; f < nfam; ++f) {
+    const int Rf = f == 0 ? Ra : Rb;
+    row_bytes += (size_t)nx * 2 * (Rf + 1) * (1 + sizeof(float2) * (size_t)lcap);
+  }
+  size_t budget = (size_t)32 << 30;   // level slots of one band (all families)
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 4);
+  }
+  int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
+  if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override
+  band = std::min(band, src->nrows);
+  stats.lev_cap = 0;
   uint32_t* ocnt = nullptr;
-  int* ovf = nullptr;
+  unsigned* flags = nullptr;
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
-  if ((s = T.get(sizeof(int) * 4, (void**)&ovf))) return s;
-  CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-  LAUNCH(T, K_P2C, launch_pass2<false>(op, FA.F, FB.F, src->d.nx, hlo, src->nrows, src->d.z_lo, src->d.z_hi, ocnt,
-                                       nullptr, nullptr, ovf, st));
-  CK(cudaGetLastError());
+  if ((s = T.get(64, (void**)&flags))) return s;
+  int acc = src->p2_acc > 0 ? src->p2_acc : 24;
+  float2* stage = nullptr;
+  for (int attempt = 0;; ++attempt) {
+    if ((s = T.get(sizeof(float2) * (size_t)pass2_stage_cap(op, acc) * ncol + 16, (void**)&stage))) return s;
+    CK(cudaMemsetAsync(flags, 0, 64, st));
+    stats.n_mid = 0;
+    stats.n_lev = 0;
+    for (int b0 = 0; b0 < src->nrows; b0 += band) {
+      const int b1 = std::min(src->nrows, b0 + band);
+      const int lr0 = std::max(0, hlo + b0 - Rmax), lr1 = std::min(nrows_ext, hlo + b1 + Rmax);
+      LevelSlots LA{}, LB{};
+      // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
+      if ((s = run_levels(src, T, rows, Ra, htab_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
+                          &stats.n_lev))) {
+        set_empty(dst);
+        return s;
+      }
+      if (op == OP_SHELL) {
+        if ((s = run_levels(src, T, rows, Rb, htab_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev))) {
+          set_empty(dst);
+          return s;
+        }
+      } else {
+        LB = LA;
+      }
+      stats.lev_cap = std::max<uint32_t>(stats.lev_cap, std::max(LA.cap, LB.cap));
+      const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, flags};
+      LAUNCH(T, K_P2, launch_pass2(op, LA, LB, nx, hlo + b0, b1 - b0, src->d.z_lo, src->d.z_hi, O, st));
+      CK(cudaGetLastError());
+      for (LevelSlots* Lf : {&LA, &LB}) {
+        if (Lf == &LB && op != OP_SHELL) break;
+        T.release(Lf->z);
+        T.release(Lf->cnt);
+        T.release(Lf->ovf_idx);
+        if (Lf->ovf_z) T.release(Lf->ovf_z);
+      }
+    }
+    unsigned hf[4];
+    CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hf[2] == 0) break;
+    // a pass-2 union outgrew the accumulator: rerun the op with a larger one
+    T.release(stage);
+    const int need = (int)hf[2];
+    int nacc = acc;
+    while (nacc < need) nacc *= 2;
+    if (pass2_smem_bytes(op, nacc, 32) > 220 * 1024) {
+      set_empty(dst);
+      return fail(DEXEL_EOVERFLOW, "a column's pass-2 union exceeds the shared-memory accumulator (" +
+                                       std::to_string(need) + " intervals)");
+    }
+    acc = nacc;
+    src->p2_acc = acc;
+    if (attempt > 8) return fail(DEXEL_ECUDA, "pass-2 accumulator sizing did not converge");
+  }
+  stats.bands = (uint32_t)((src->nrows + band - 1) / band);
+  stats.p2_acc = acc;
   uint64_t nout = 0;
-  // dst offsets: reuse dst->off
   if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
   if ((s = scan_counts(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p, &nout))) return s;
-  int hovf = 0;
-  CK(cudaMemcpy(&hovf, ovf, sizeof(int), cudaMemcpyDeviceToHost));
-  if (hovf) {
-    set_empty(dst);
-    return fail(DEXEL_EOVERFLOW, "a column's union exceeds the pass-2 accumulator (" + std::to_string(ACC_CAP) +
-                                     " intervals)");
-  }
   dfree(dst, dst->ep);
   if ((s = dalloc(dst, dst->ep, sizeof(float2) * (nout + 1)))) return s;
-  LAUNCH(T, K_P2W, launch_pass2<true>(op, FA.F, FB.F, src->d.nx, hlo, src->nrows, src->d.z_lo, src->d.z_hi,
-                                      nullptr, (const uint64_t*)dst->off.p, (float2*)dst->ep.p, ovf, st));
+  if (ncol > 0)
+    LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(
+                             stage, ocnt, (const uint64_t*)dst->off.p, ncol, (float2*)dst->ep.p));
   CK(cudaGetLastError());
   dst->n = nout;
   stats.n_out = nout;
@@ -599,6 +621,9 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
   }
   dexel_grid g = new dexel_grid_s();
   g->d = *d;
+  // initial capacity hints (testing / tuning overrides; grown automatically on overflow)
+  if (const char* e = std::getenv("DEXEL_LEV_CAP")) g->lev_cap = std::max(1, std::min(255, std::atoi(e)));
+  if (const char* e = std::getenv("DEXEL_P2_ACC")) g->p2_acc = std::max(1, std::atoi(e));
   g->nrows = d->y1 - d->y0;
   g->ncol = (int64_t)g->nrows * d->nx;
   if (d->stream) {

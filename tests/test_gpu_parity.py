@@ -241,10 +241,11 @@ def test_torch_allocator_hook(dx):
 
 
 
-def test_levels_envelope_variant_matches(dx):
-    """The alternative level-set kernel (explicit upper envelope of the power functions,
-    DEXEL_LEVELS=envelope) agrees with the oracle too.  Subprocess: the mode is read once
-    per process."""
+def test_capacity_regrowth(dx):
+    """Start every capacity at its minimum (level slots per list, pass-2 accumulator:
+    DEXEL_LEV_CAP / DEXEL_P2_ACC) so every op overflows and reruns with grown
+    capacities, and cut the grid into 3-row bands (DEXEL_BAND_ROWS); results still
+    match the oracle.  Subprocess: the hints are read when a handle is created."""
     import os
     import subprocess
     import sys
@@ -252,25 +253,30 @@ def test_levels_envelope_variant_matches(dx):
 import sys; sys.path.insert(0, %r)
 import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
 from oracle.compare import compare
-for seed in range(16):
+for seed in range(12):
     rs = np.random.default_rng(77 + seed)
-    host = G.random_grid(int(rs.integers(2, 40)), int(rs.integers(2, 30)), 4, -12.0, 12.0, seed)
+    host = G.random_grid(int(rs.integers(2, 40)), int(rs.integers(2, 30)), 6, -12.0, 12.0, seed)
     r = float(rs.choice([1.0, 2.5, 4.0, 7.0, 16.0, 20.0, 40.0]))
     src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
-    for op in ("dilate", "erode"):
-        getattr(dx, "dexel_" + op)(src, r, dst); off, ep = dst.download(); ref = getattr(O, op)(host, r)
+    for op in ("dilate", "erode", "shell"):
+        if op == "shell":
+            dx.dexel_shell(src, r, r, dst); ref = O.shell(host, r, r)
+        else:
+            getattr(dx, "dexel_" + op)(src, r, dst); ref = getattr(O, op)(host, r)
+        off, ep = dst.download()
         res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (op, r, res)
 print("OK")
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DEXEL_LEVELS="envelope")
+    env = dict(os.environ, DEXEL_LEV_CAP="1", DEXEL_P2_ACC="1", DEXEL_BAND_ROWS="3")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
 
 
 @pytest.mark.parametrize("op", ["dilate", "erode", "shell"])
 def test_many_intervals_fallback(dx, op):
-    """Columns whose result holds more intervals than the shared-memory accumulator
-    (ACC_S = 32) take the local-memory pass-2 kernel; results still match the oracle."""
+    """Columns whose level sets and unions hold more intervals than the default
+    capacities (8 per level list, 24 per pass-2 union) make the op rerun with grown
+    capacities; results still match the oracle."""
     col = [(float(t) * 0.5 - 40.0, float(t) * 0.5 - 39.8) for t in range(120)]   # 120 thin layers
     cols = [col if (i + j) % 3 == 0 else [] for j in range(4) for i in range(5)]
     host = _grid(5, 4, cols, -41.0, 41.0)

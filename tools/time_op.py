@@ -35,3 +35,5 @@ for timing in (False, True):
     st = dst.stats()
     print(f"{cfg} {op} r={r} timing={timing}: wall {1e3*dt:.2f} ms/op; kernels "
           f"{sum(st['kernel_ms'].values()):.2f} ms {({k: round(v, 2) for k, v in st['kernel_ms'].items()})}")
+print(f"  n_in={st['n_in']} n_mid={st['n_mid']} n_lev={st['n_lev']} n_out={st['n_out']} launches={st['launches']} "
+      f"capacities={st['capacities']}")
