@@ -298,26 +298,32 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   const unsigned ovf_cap = (unsigned)std::max<int64_t>(256, ncol / 256);
   uint32_t* ovf_list = nullptr;
   if ((s = T.get(sizeof(uint32_t) * ovf_cap, (void**)&ovf_list))) return s;
-  // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of <= 24
-  static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17, 20, 24};
-  const int nchunk = (R + 1 + 23) / 24;
+  // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of
+  // <= max_chunk (larger chunks cost more in registers/occupancy than they save)
+  static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17};
+  int max_chunk = 12;   // measured on B200: 12 <= 17 < 9 at r = 64, equal at r = 16
+  if (const char* e = std::getenv("DEXEL_LV_CHUNK")) max_chunk = std::max(2, std::min(17, std::atoi(e)));
+  const int nchunk = (R + 1 + max_chunk - 1) / max_chunk;
   const int per = (R + 1 + nchunk - 1) / nchunk;
-  int lmax = 24;
+  int lmax = 17;
   for (int v : kChunk)
     if (v >= per) { lmax = v; break; }
   auto launch = [&](const LvArgs& A, int64_t nwork) {
-    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk);
     if (nwork <= 0) return;
+    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk);
     T.prof.pre(K_LEV);
     switch (lmax) {
 #define LV(V) case V: levels_kernel<V><<<grid, LV_T, 0, g->stream>>>(A); break;
-      LV(2) LV(3) LV(4) LV(5) LV(6) LV(8) LV(10) LV(12) LV(14) LV(17) LV(20) LV(24)
+      LV(2) LV(3) LV(4) LV(5) LV(6) LV(8) LV(10) LV(12) LV(14) LV(17)
 #undef LV
     }
     T.prof.post();
   };
   for (int attempt = 0; attempt < 6; ++attempt) {
-    if ((s = T.get(sizeof(float2) * nlist * L->cap + 16, (void**)&L->z))) return s;
+    const size_t nslot = (size_t)ncol * 2 * (R + 2) * L->cap;   // + the spill level per (row, d)
+    if ((size_t)(R + 2) * L->cap * src.nx >= (1ull << 32))
+      return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
+    if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
     CK(cudaMemsetAsync(flags, 0, 64, g->stream));
     LvArgs A{P.moff, P.mz, P.mk, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, ovf_list, ovf_cap, nullptr, 0};
     launch(A, ncol);
@@ -485,7 +491,7 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   size_t row_bytes = 0;   // level-slot bytes per level row, all families
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
-    row_bytes += (size_t)nx * 2 * (Rf + 1) * (1 + sizeof(float2) * (size_t)lcap);
+    row_bytes += (size_t)nx * 2 * ((Rf + 1) + (Rf + 2) * sizeof(float2) * (size_t)lcap);
   }
   size_t budget = (size_t)32 << 30;   // level slots of one band (all families)
   {
@@ -500,7 +506,7 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   unsigned* flags = nullptr;
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
   if ((s = T.get(64, (void**)&flags))) return s;
-  int acc = src->p2_acc > 0 ? src->p2_acc : 24;
+  int acc = src->p2_acc > 0 ? src->p2_acc : 32;
   float2* stage = nullptr;
   for (int attempt = 0;; ++attempt) {
     if ((s = T.get(sizeof(float2) * (size_t)pass2_stage_cap(op, acc) * ncol + 16, (void**)&stage))) return s;

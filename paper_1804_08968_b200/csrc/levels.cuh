@@ -26,7 +26,7 @@
 // 4-6x slower: 4 of 32 lanes active per instruction.)
 //
 // Layout (HBM): level slots, direction d = 0 (U_f, ascending) / 1 (U_r, stored
-// descending):  z[(((row*2 + d)*(R+1) + k)*cap + t)*nx + i]  (float2), counts
+// descending):  z[(((row*2 + d)*cap + t)*(R+2) + k)*nx + i]  (float2), counts
 // cnt[((row*2 + d)*(R+1) + k)*nx + i] (u8).  For a fixed (row, d, k, t) the nx
 // columns of a row are contiguous, so a warp of 32 consecutive columns writes
 // and (in pass 2) reads 256 contiguous bytes.  A list longer than cap raises a
@@ -44,7 +44,7 @@ constexpr int LV_OVF_CAP = 255;   // list capacity in the overflow arena (counts
 
 struct LevelSlots {
   uint8_t* cnt;      // [nrows][2][R+1][nx]  true list lengths (<= 255)
-  float2* z;         // [nrows][2][R+1][cap][nx]
+  float2* z;         // [nrows][2][cap][R+2][nx]  (unclipped; level R+1 of the last slot = spill cell)
   int R, cap, nx, nrows;
   int row0;          // row (in the op's extended-row numbering) of slot row 0
   // columns with a list longer than cap keep all their lists in the overflow arena:
@@ -56,8 +56,12 @@ struct LevelSlots {
 __host__ __device__ __forceinline__ size_t slot_cnt_index(const LevelSlots& L, int row, int d, int k, int i) {
   return (((size_t)row * 2 + d) * (L.R + 1) + k) * L.nx + i;
 }
+// z slots, slot-major inside a (row, d) block: z[(((row*2 + d)*cap + t)*(R+2) + k)*nx + i].
+// Level R+1 of the last slot is a spill cell: an emission is written at
+// min(offset, spill), so an overflowing list (t >= cap) only ever hits the spill cell
+// (its column is then redone in the overflow arena) and never another list.
 __host__ __device__ __forceinline__ size_t slot_z_index(const LevelSlots& L, int row, int d, int k, int t, int i) {
-  return ((((size_t)row * 2 + d) * (L.R + 1) + k) * L.cap + t) * L.nx + i;
+  return ((((size_t)row * 2 + d) * L.cap + t) * (L.R + 2) + k) * L.nx + i;
 }
 
 __host__ __device__ __forceinline__ size_t ovf_z_index(const LevelSlots& L, int q, int d, int k, int t) {
@@ -82,38 +86,31 @@ struct LvArgs {
 
 constexpr int LV_T = 128;
 
-// q < 0: main pass (slots); q >= 0: overflow pass (arena slot q)
-__device__ __forceinline__ void lv_emit(const LvArgs& A, int q, int row, int d, int k, int i, uint32_t& n, float lo,
-                                        float hi) {
-  lo = fmaxf(lo, A.zlo);
-  hi = fminf(hi, A.zhi);
-  if (lo < hi) {
-    if (q < 0) {
-      if (n < (uint32_t)A.L.cap) A.L.z[slot_z_index(A.L, row, d, k, (int)n, i)] = make_float2(lo, hi);
-    } else if (n < (uint32_t)LV_OVF_CAP) {
-      A.L.ovf_z[ovf_z_index(A.L, q, d, k, (int)n)] = make_float2(lo, hi);
-    }
-    ++n;
-  }
-}
-
 // blockIdx.y = level chunk: this thread runs levels k0 .. k0+LMAX-1 of column c.
-// The h table rows are HS = LMAX | 1 floats apart: an odd stride puts the rows of
-// different kappa (the lanes' pieces differ) in different banks.
+// The h table holds -inf where a piece is out of reach (kappa^2 + k^2 > (r/s)^2): then
+// hi + h = -inf and lo - h = +inf leave the running union unchanged without a validity
+// test, and a "break" by such a piece only closes a component that no later piece (all
+// start higher) could extend anyway.  Rows are HS floats (HS/4 odd): a row is read with
+// 128-bit loads, and 8 lanes with different kappa hit 8 different bank groups.
 template <int LMAX>
-__global__ void __launch_bounds__(LV_T) levels_kernel(LvArgs A) {
-  constexpr int HS = LMAX | 1;
-  __shared__ float Hs[256 * HS];          // h(kappa, k0 + k), -1 beyond R or invalid
-  __shared__ unsigned long long blk_total;
-  __shared__ unsigned blk_max;
+struct LvTab {
+  static constexpr int NV = (LMAX + 3) / 4;                 // float4 per row actually used
+  static constexpr int HS = 4 * (NV | 1);                   // row stride (floats), HS/4 odd
+};
+
+template <int LMAX>
+__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs A) {
+  constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
+  __shared__ __align__(16) float Hs[256 * HS];   // h(kappa, k0 + k), -inf beyond R or out of reach
   const int R = A.L.R, L1 = R + 1;
   const int k0 = blockIdx.y * LMAX;
   for (int t = threadIdx.x; t < L1 * HS; t += LV_T) {
-    const int kap = t / HS, k = k0 + t % HS;
-    Hs[t] = (k <= R && t % HS < LMAX) ? A.h[kap * L1 + k] : -1.0f;
+    const int kap = t / HS, kk = t % HS, k = k0 + kk;
+    const float h = (kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
+    Hs[t] = h >= 0.f ? h : -INFINITY;
   }
-  if (threadIdx.x == 0) { blk_total = 0; blk_max = 0; }
   __syncthreads();
+  uint32_t tot = 0, mx = 0;
   const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
   if (g < (A.list ? A.nlist : A.ncol)) {
     const int64_t c = A.list ? (int64_t)A.list[g] : g;
@@ -122,76 +119,85 @@ __global__ void __launch_bounds__(LV_T) levels_kernel(LvArgs A) {
     const uint64_t base = A.moff[c];
     const int m = (int)(A.moff[c + 1] - base);
     float a[LMAX], b[LMAX];
-    uint32_t n[LMAX];
-    uint32_t tot = 0, mx = 0;
-    // ---- U_f: forward running union of [lo, hi + h]
+    uint32_t o[LMAX];   // next slot of level k0+k, as a float2 offset from slot 0 / level k0 of the block
+    const uint32_t nx = (uint32_t)A.L.nx, S = (uint32_t)(R + 2) * nx;      // S = one slot (all levels)
+    const uint32_t omax = (uint32_t)(A.L.cap - 1) * S + (uint32_t)(R + 1 - k0) * nx;   // the spill cell
 #pragma unroll
-    for (int k = 0; k < LMAX; ++k) { a[k] = 0.f; b[k] = -INFINITY; n[k] = 0; }
-    {
-      float2 nz = m > 0 ? A.mz[base] : make_float2(0.f, 0.f);
-      int nk = m > 0 ? A.mk[base] : 0;
+    for (int d = 0; d < 2; ++d) {
+      // main pass: slots of (row, d, level k0); overflow pass: the arena lists of slot q
+      float2* Zd = q < 0 ? A.L.z + slot_z_index(A.L, row, d, k0, 0, i)
+                         : A.L.ovf_z + ovf_z_index(A.L, q, d, k0, 0);
+      const uint32_t ostep = q < 0 ? S : 1u, olev = q < 0 ? nx : (uint32_t)LV_OVF_CAP;
+      const uint32_t olim = q < 0 ? omax : (uint32_t)(R + 1 - k0) * LV_OVF_CAP - 1u;
+#pragma unroll
+      for (int k = 0; k < LMAX; ++k) {
+        a[k] = d ? INFINITY : 0.f;
+        b[k] = d ? 0.f : -INFINITY;
+        o[k] = (uint32_t)k * olev;
+      }
+      // emission: closed component [a, b] of level k (empty placeholders have a >= b);
+      // branch-free -- a predicated store, the slot clamped into the spill zone
+#define LV_EMIT(k, pred)                                                      \
+  {                                                                           \
+    const bool ok_ = (pred) && a[k] < b[k];                                   \
+    if (ok_) Zd[min(o[k], olim)] = make_float2(a[k], b[k]);                   \
+    o[k] += ok_ ? ostep : 0u;                                                 \
+  }
+      float2 nz = m > 0 ? A.mz[base + (d ? m - 1 : 0)] : make_float2(0.f, 0.f);
+      int nk = m > 0 ? A.mk[base + (d ? m - 1 : 0)] : 0;
+      float2 nz2 = m > 1 ? A.mz[base + (d ? m - 2 : 1)] : make_float2(0.f, 0.f);
+      int nk2 = m > 1 ? A.mk[base + (d ? m - 2 : 1)] : 0;
       for (int t = 0; t < m; ++t) {
         const float2 p = nz;
-        const float* hrow = Hs + nk * HS;
-        if (t + 1 < m) { nz = A.mz[base + t + 1]; nk = A.mk[base + t + 1]; }   // prefetch
-        if (hrow[0] < 0.f) continue;        // validity is monotone in k: the whole chunk is out of reach
+        const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
+        nz = nz2; nk = nk2;
+        if (t + 2 < m) {
+          const uint64_t idx = base + (d ? (uint64_t)(m - 3 - t) : (uint64_t)(t + 2));
+          nz2 = A.mz[idx]; nk2 = A.mk[idx];
+        }
+        float hv[4 * NV];
 #pragma unroll
-        for (int k = 0; k < LMAX; ++k) {
-          const float h = hrow[k];
-          const bool valid = h >= 0.f;
-          const bool brk = valid && p.x > b[k];
-          if (brk) lv_emit(A, q, row, 0, k0 + k, i, n[k], a[k], b[k]);   // b = -inf emits nothing
-          a[k] = brk ? p.x : a[k];
-          const float e = p.y + h;
-          b[k] = valid ? (brk ? e : fmaxf(b[k], e)) : b[k];
+        for (int j = 0; j < NV; ++j) {
+          const float4 v = hrow[j];
+          hv[4 * j] = v.x; hv[4 * j + 1] = v.y; hv[4 * j + 2] = v.z; hv[4 * j + 3] = v.w;
+        }
+        if (hv[0] == -INFINITY) continue;   // reach is monotone in k: the whole chunk is out of reach
+        if (d == 0) {                        // U_f: forward running union of [lo, hi + h]
+#pragma unroll
+          for (int k = 0; k < LMAX; ++k) {
+            const bool brk = p.x > b[k];
+            LV_EMIT(k, brk);
+            a[k] = brk ? p.x : a[k];
+            const float e = p.y + hv[k];
+            b[k] = brk ? e : fmaxf(b[k], e);
+          }
+        } else {                             // U_r: backward running union of [lo - h, hi]
+#pragma unroll
+          for (int k = 0; k < LMAX; ++k) {
+            const bool brk = p.y < a[k];
+            LV_EMIT(k, brk);
+            b[k] = brk ? p.y : b[k];
+            const float st = p.x - hv[k];
+            a[k] = brk ? st : fminf(a[k], st);
+          }
         }
       }
 #pragma unroll
       for (int k = 0; k < LMAX; ++k) {
-        lv_emit(A, q, row, 0, k0 + k, i, n[k], a[k], b[k]);
+        LV_EMIT(k, true);
+#undef LV_EMIT
         if (k0 + k <= R) {
-          A.L.cnt[slot_cnt_index(A.L, row, 0, k0 + k, i)] = (uint8_t)min(n[k], 255u);
-          tot += n[k];
-          mx = max(mx, n[k]);
+          const uint32_t nk_ = (o[k] - (uint32_t)k * olev) / ostep;
+          if (q < 0) A.L.cnt[slot_cnt_index(A.L, row, d, k0 + k, i)] = (uint8_t)min(nk_, 255u);
+          tot += nk_;
+          mx = max(mx, nk_);
         }
       }
     }
-    // ---- U_r: backward running union of [lo - h, hi]; stored in descending order
-#pragma unroll
-    for (int k = 0; k < LMAX; ++k) { a[k] = INFINITY; b[k] = 0.f; n[k] = 0; }
-    {
-      float2 nz = m > 0 ? A.mz[base + m - 1] : make_float2(0.f, 0.f);
-      int nk = m > 0 ? A.mk[base + m - 1] : 0;
-      for (int t = m - 1; t >= 0; --t) {
-        const float2 p = nz;
-        const float* hrow = Hs + nk * HS;
-        if (t > 0) { nz = A.mz[base + t - 1]; nk = A.mk[base + t - 1]; }
-        if (hrow[0] < 0.f) continue;
-#pragma unroll
-        for (int k = 0; k < LMAX; ++k) {
-          const float h = hrow[k];
-          const bool valid = h >= 0.f;
-          const bool brk = valid && p.y < a[k];
-          if (brk) lv_emit(A, q, row, 1, k0 + k, i, n[k], a[k], b[k]);   // a = +inf emits nothing
-          b[k] = brk ? p.y : b[k];
-          const float st = p.x - h;
-          a[k] = valid ? (brk ? st : fminf(a[k], st)) : a[k];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < LMAX; ++k) {
-        lv_emit(A, q, row, 1, k0 + k, i, n[k], a[k], b[k]);
-        if (k0 + k <= R) {
-          A.L.cnt[slot_cnt_index(A.L, row, 1, k0 + k, i)] = (uint8_t)min(n[k], 255u);
-          tot += n[k];
-          mx = max(mx, n[k]);
-        }
-      }
-    }
-    if (q < 0) atomicAdd(&blk_total, (unsigned long long)tot);   // the overflow pass recounts nothing
+    if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
     if (mx > (unsigned)A.L.cap) {
-      atomicMax(&blk_max, mx);
-      if (q < 0) {                                                  // hand the column to the overflow pass
+      atomicMax(A.flags, mx);
+      if (q < 0) {                          // hand the column to the overflow pass
         const unsigned slot = atomicAdd(A.flags + 1, 1u);
         if (slot < A.ovf_list_cap) {
           A.ovf_list[slot] = (uint32_t)c;
@@ -200,11 +206,9 @@ __global__ void __launch_bounds__(LV_T) levels_kernel(LvArgs A) {
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (A.nlev) atomicAdd(A.nlev, blk_total);
-    if (blk_max) atomicMax(A.flags, blk_max);
-  }
+  // statistics: one atomic per warp, no block barrier (warps retire independently)
+  const unsigned wsum = __reduce_add_sync(0xffffffffu, tot);
+  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(A.nlev, (unsigned long long)wsum);
 }
 
 }  // namespace dexel

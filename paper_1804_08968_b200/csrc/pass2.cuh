@@ -11,9 +11,9 @@
 //
 // One thread per output column; a warp covers 32 consecutive columns of a row,
 // so every list read (fixed row, level, slot t) is a coalesced 256-byte access.
-// The running union lives in shared memory ([slot][thread], conflict-free),
-// ping-ponged between two buffers per family; a union longer than `acc`
-// raises a flag and the host reruns with a larger accumulator.  Results go to a
+// The running union lives in shared memory ([slot][thread], conflict-free) and is
+// updated in place (acc_insert); a union longer than `acc` raises a flag and the
+// host reruns with a larger accumulator.  Results go to a
 // [t][column] staging array; compact_kernel moves them into the output CSR once
 // the counts are scanned (two-phase allocation without recomputation).
 #pragma once
@@ -26,80 +26,104 @@ namespace dexel {
 
 enum { OP_DILATE = 0, OP_ERODE = 1, OP_SHELL = 2 };
 
-// merge the running union A (smem, stride T) with sorted list B (global, element t at
-// B[t * bstride]; bstride < 0 walks a list stored in descending order) into O
+// In-place running union: acc[0..n) (shared memory, stride T) holds sorted disjoint closed
+// intervals.  Elements of one sorted list are inserted in order with a monotone cursor:
+// an element inside an accumulator interval costs a compare (the common case -- most of
+// the 4R+2 lists of a column fall inside what L_0 and the near rows already cover); an
+// element that reaches outside merges the overlapped run of intervals and shifts the tail.
+// Returns the new count (> cap: overflow, contents truncated).
+struct Acc {
+  float2* v;   // v[t * T]
+  int n;
+};
+
 template <int T>
-__device__ __forceinline__ int p2_merge(const float2* A, int na, const float2* __restrict__ B, int nb,
-                                        int64_t bstride, float2* O, int acc) {
-  int ia = 0, ib = 0, no = 0;
-  float cs = 0.f, ce = 0.f;
-  bool have = false;
-  float2 xa = na > 0 ? A[0] : make_float2(INFINITY, INFINITY);
-  float2 xb = nb > 0 ? B[0] : make_float2(INFINITY, INFINITY);
-  while (ia < na || ib < nb) {
-    float2 x;
-    if (ib >= nb || (ia < na && xa.x <= xb.x)) {
-      x = xa;
-      ++ia;
-      if (ia < na) xa = A[ia * T];
-    } else {
-      x = xb;
-      ++ib;
-      if (ib < nb) xb = B[(int64_t)ib * bstride];
-    }
-    if (!have) {
-      cs = x.x; ce = x.y; have = true;
-    } else if (x.x <= ce) {
-      ce = fmaxf(ce, x.y);
-    } else {
-      if (no < acc) O[no * T] = make_float2(cs, ce);
-      ++no;
-      cs = x.x; ce = x.y;
+__device__ __forceinline__ void acc_insert(Acc& A, int& p, float a, float b, int cap, unsigned* need) {
+  // p: first index with v[p].y >= a (monotone over one list, since the list's starts increase)
+  while (p < A.n && A.v[p * T].y < a) ++p;
+  if (p < A.n) {
+    const float2 w = A.v[p * T];
+    if (w.x <= a && b <= w.y) return;                 // covered
+    if (w.x <= b) {                                   // overlaps [w.x, w.y]: merge the run p..q
+      int q = p;
+      float e = fmaxf(b, w.y);
+      while (q + 1 < A.n && A.v[(q + 1) * T].x <= e) { ++q; e = fmaxf(e, A.v[q * T].y); }
+      A.v[p * T] = make_float2(fminf(a, w.x), e);
+      const int drop = q - p;
+      if (drop) {
+        for (int t = q + 1; t < A.n; ++t) A.v[(t - drop) * T] = A.v[t * T];
+        A.n -= drop;
+      }
+      return;
     }
   }
-  if (have) {
-    if (no < acc) O[no * T] = make_float2(cs, ce);
-    ++no;
+  // disjoint from everything: insert before p (shift the tail right)
+  if (A.n >= cap) { *need = max(*need, (unsigned)(A.n + 1)); return; }
+  for (int t = A.n; t > p; --t) A.v[t * T] = A.v[(t - 1) * T];
+  A.v[p * T] = make_float2(a, b);
+  ++A.n;
+}
+
+constexpr int P2_R = 8;   // list elements loaded into registers per batch
+
+// insert a sorted list (element e at B[e * stride]) into the accumulator, P2_R elements at a
+// time: the batch's loads are independent and issue together
+// (level sets are stored unclipped: each element is clipped to [zlo, zhi] here; clipping
+// commutes with the union)
+template <int T>
+__device__ __forceinline__ void acc_insert_list(Acc& A, const float2* __restrict__ B, int nb, int64_t stride,
+                                                float zlo, float zhi, int cap, unsigned* need) {
+  int p = 0;
+  for (int e0 = 0; e0 < nb; e0 += P2_R) {
+    float2 x[P2_R];
+#pragma unroll
+    for (int u = 0; u < P2_R; ++u)
+      if (e0 + u < nb) x[u] = B[(int64_t)(e0 + u) * stride];
+#pragma unroll
+    for (int u = 0; u < P2_R; ++u) {
+      if (e0 + u >= nb) continue;
+      const float lo = fmaxf(x[u].x, zlo), hi = fminf(x[u].y, zhi);
+      if (lo < hi) acc_insert<T>(A, p, lo, hi, cap, need);
+    }
   }
-  return no;
 }
 
 // union over dy of one family's level lists for output column (i, jg): for each row
-// offset, U_f(|dy|) (ascending) and U_r(|dy|) (stored descending) of column (i, jg+dy).
-// Returns the count; *res = the buffer holding it (X or Y).
+// offset dy = 0, 1, -1, 2, -2, ... the lists U_f(|dy|) (ascending) and U_r(|dy|) (stored
+// descending) of column (i, jg+dy); the two counts of the next row are loaded ahead.
 template <int T>
-__device__ __forceinline__ int p2_family(const LevelSlots& L, int i, int jg, float2* X, float2* Y, int acc,
-                                         float2** res, unsigned* need) {
-  int na = 0;
-  float2* cur = X;
-  float2* nxt = Y;
-  for (int t = 0; t <= 2 * L.R; ++t) {
-    const int dy = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);   // 0, 1, -1, 2, -2, ...
-    const int jl = jg + dy - L.row0;
-    if (jl < 0 || jl >= L.nrows) continue;
-    const int k = dy < 0 ? -dy : dy;
+__device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A, int cap,
+                                          unsigned* need) {
+  A.n = 0;
+  const int dlo = max(-L.R, L.row0 - jg), dhi = min(L.R, L.row0 + L.nrows - 1 - jg);
+  const int nt = 2 * L.R + 1;
+  auto dy_of = [](int t) { return (t & 1) ? ((t + 1) >> 1) : -(t >> 1); };
+  auto count = [&](int t, int d) -> int {
+    if (t >= nt) return 0;
+    const int dy = dy_of(t), k = dy < 0 ? -dy : dy;
+    return (dy < dlo || dy > dhi) ? 0 : L.cnt[slot_cnt_index(L, jg + dy - L.row0, d, k, i)];
+  };
+  int c0 = count(0, 0), c1 = count(0, 1);
+  for (int t = 0; t < nt; ++t) {
+    const int n0 = c0, n1 = c1;
+    c0 = count(t + 1, 0);
+    c1 = count(t + 1, 1);
+    if (n0 + n1 == 0) continue;
+    const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
-      const int nb = L.cnt[slot_cnt_index(L, jl, d, k, i)];
+      const int nb = d ? n1 : n0;
       if (nb == 0) continue;
-      const float2* lb;
-      int64_t stride;
       if (nb <= L.cap) {
-        lb = L.z + slot_z_index(L, jl, d, k, d ? nb - 1 : 0, i);
-        stride = d ? -(int64_t)L.nx : (int64_t)L.nx;
+        const int64_t ts = (int64_t)(L.R + 2) * L.nx;   // one slot
+        acc_insert_list<T>(A, L.z + slot_z_index(L, jl, d, k, d ? nb - 1 : 0, i), nb, d ? -ts : ts, zlo, zhi, cap,
+                           need);
       } else {   // the column's lists live in the overflow arena
         const int q = L.ovf_idx[(size_t)jl * L.nx + i];
-        lb = L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0);
-        stride = d ? -1 : 1;
+        acc_insert_list<T>(A, L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0), nb, d ? -1 : 1, zlo, zhi, cap, need);
       }
-      const int n = p2_merge<T>(cur, na, lb, nb, stride, nxt, acc);
-      if (n > acc) { *need = max(*need, (unsigned)n); na = acc; }
-      else na = n;
-      float2* tmp = cur; cur = nxt; nxt = tmp;
     }
   }
-  *res = cur;
-  return na;
 }
 
 // output rows [row0, row0 + nrows_out) (extended-row numbering of the level slots) of a band;
@@ -116,35 +140,39 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
   if (cl >= (int64_t)nrows_out * nx) return;
   const int64_t c = cbase + cl;
   const int i = (int)(cl % nx), jg = row0 + (int)(cl / nx);
-  float2* b0 = p2_smem + tid;
-  float2* b1 = b0 + acc * T;
-  float2* b2 = b1 + acc * T;
   unsigned need = 0;
-  float2* ra;
-  const int na = p2_family<T>(A, i, jg, b0, b1, acc, &ra, &need);
+  Acc U{p2_smem + tid, 0};
+  p2_family<T>(A, i, jg, zlo, zhi, U, acc, &need);
   uint32_t n = 0;
   if (OP == OP_DILATE) {
-    for (int t = 0; t < na; ++t) ostage[(size_t)t * ncol + c] = ra[t * T];
-    n = na;
+    for (int t = 0; t < U.n; ++t) ostage[(size_t)t * ncol + c] = U.v[t * T];
+    n = U.n;
   } else if (OP == OP_ERODE) {
     float cur = zlo;
-    for (int t = 0; t < na; ++t) {
-      const float2 v = ra[t * T];
+    for (int t = 0; t < U.n; ++t) {
+      const float2 v = U.v[t * T];
       if (v.x > cur) ostage[(size_t)(n++) * ncol + c] = make_float2(cur, v.x);
       cur = v.y;
     }
     if (zhi > cur) ostage[(size_t)(n++) * ncol + c] = make_float2(cur, zhi);
-  } else {
-    // family B uses the two buffers not holding A's result
-    float2* x = ra == b0 ? b1 : b0;
-    float2* rb;
-    const int nbb = p2_family<T>(B, i, jg, x, b2, acc, &rb, &need);
+  } else {   // shell: D_rout(S) n D_rin(C)
+    // park D_rout(S) in the upper half of this column's staging slots (coalesced), reuse the
+    // shared accumulator for D_rin(C), then intersect into the lower half (the result has
+    // at most |U| + |V| - 1 <= 2 acc - 1 intervals and is written behind the reads)
+    const int nu = U.n;
+    for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * T];
+    p2_family<T>(B, i, jg, zlo, zhi, U, acc, &need);
     int p = 0, q = 0;
-    while (p < na && q < nbb) {
-      const float2 u = ra[p * T], v = rb[q * T];
+    float2 u = nu > 0 ? ostage[(size_t)acc * ncol + c] : make_float2(0.f, 0.f);
+    while (p < nu && q < U.n) {
+      const float2 v = U.v[q * T];
       const float lo = fmaxf(u.x, v.x), hi = fminf(u.y, v.y);
       if (lo < hi) ostage[(size_t)(n++) * ncol + c] = make_float2(lo, hi);
-      if (u.y < v.y) ++p; else ++q;
+      if (u.y < v.y) {
+        if (++p < nu) u = ostage[(size_t)(acc + p) * ncol + c];
+      } else {
+        ++q;
+      }
     }
   }
   ocnt[c] = n;
@@ -152,7 +180,8 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
 }
 
 inline size_t pass2_smem_bytes(int op, int acc, int T) {
-  return (size_t)(op == OP_SHELL ? 3 : 2) * acc * T * sizeof(float2);
+  (void)op;
+  return (size_t)acc * T * sizeof(float2);
 }
 inline int pass2_stage_cap(int op, int acc) { return op == OP_SHELL ? 2 * acc : acc + 1; }
 

@@ -241,7 +241,8 @@ def test_torch_allocator_hook(dx):
 
 
 
-def test_capacity_regrowth(dx):
+@pytest.mark.parametrize("lev_cap,acc,band", [("1", "1", "3"), ("2", "4", "7")])
+def test_capacity_regrowth(dx, lev_cap, acc, band):
     """Start every capacity at its minimum (level slots per list, pass-2 accumulator:
     DEXEL_LEV_CAP / DEXEL_P2_ACC) so every op overflows and reruns with grown
     capacities, and cut the grid into 3-row bands (DEXEL_BAND_ROWS); results still
@@ -267,7 +268,7 @@ for seed in range(12):
         res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (op, r, res)
 print("OK")
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DEXEL_LEV_CAP="1", DEXEL_P2_ACC="1", DEXEL_BAND_ROWS="3")
+    env = dict(os.environ, DEXEL_LEV_CAP=lev_cap, DEXEL_P2_ACC=acc, DEXEL_BAND_ROWS=band)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
 
