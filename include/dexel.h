@@ -143,7 +143,8 @@ const char* dexel_last_error(void);
 
 /* Route device allocations through a caller allocator (e.g. the PyTorch
  * caching allocator).  NULL,NULL restores cudaMallocAsync/cudaFreeAsync.
- * Must be called while no handle holds memory. */
+ * Each buffer is released by the allocator that produced it, so the hook may
+ * change while handles hold memory (the callbacks must outlive those buffers). */
 typedef void* (*dexel_alloc_fn)(size_t bytes, int device, void* stream, void* ctx);
 typedef void (*dexel_free_fn)(void* ptr, size_t bytes, int device, void* stream, void* ctx);
 dexel_status dexel_set_allocator(dexel_alloc_fn alloc, dexel_free_fn free_, void* ctx);
@@ -153,7 +154,7 @@ dexel_status dexel_set_allocator(dexel_alloc_fn alloc, dexel_free_fn free_, void
  * number of kernels the op launched; and, when timing is on
  * (dexel_set_timing(1)), the summed device time and launch count of each
  * kernel kind, measured with CUDA events on the handle's stream:
- *   0 pass1 count, 1 pass1 write, 2 levels (envelope), 3 pass2,
+ *   0 pass1, 1 pass1 overflow (list) launches, 2 levels, 3 pass2,
  *   4 compaction, 5 scan, 6 other, 7 reserved. */
 #define DEXEL_NKERNELS 8
 typedef struct {

@@ -44,7 +44,7 @@ class dexel_desc(ctypes.Structure):
 
 
 NKERNELS = 8
-KERNEL_NAMES = ["pass1_count", "pass1_write", "levels", "pass2", "compact", "scan", "other", "reserved"]
+KERNEL_NAMES = ["pass1", "pass1_list", "levels", "pass2", "compact", "scan", "other", "reserved"]
 
 
 class dexel_stats(ctypes.Structure):

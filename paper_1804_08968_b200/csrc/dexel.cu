@@ -51,6 +51,8 @@ dexel_status fail(dexel_status s, const std::string& msg) {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
+  dexel_free_fn freefn = nullptr;   // the allocator that produced p (NULL: cudaMallocAsync)
+  void* ctx = nullptr;
 };
 
 }  // namespace
@@ -65,7 +67,7 @@ struct dexel_grid_s {
   uint64_t n = 0;
   dexel_stats stats{};
   // capacity hints carried between ops (grown on overflow)
-  int lev_cap = 0, p2_acc = 0;
+  int lev_cap = 0, p2_acc = 0, p1_cap = 0;
   // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
   Buf hoff[2], hep[2];
   int hrows[2] = {0, 0};
@@ -84,6 +86,8 @@ dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
   b.bytes = bytes;
   b.p = nullptr;
   if (bytes == 0) bytes = 16;
+  b.freefn = g_free;
+  b.ctx = g_alloc_ctx;
   if (g_alloc) {
     b.p = g_alloc(bytes, g->d.device, (void*)g->stream, g_alloc_ctx);
     if (!b.p) return fail(DEXEL_ENOMEM, "allocator returned NULL for " + std::to_string(bytes) + " bytes");
@@ -100,14 +104,15 @@ dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
 
 void dfree(dexel_grid g, Buf& b) {
   if (!b.p) return;
-  if (g_free) g_free(b.p, b.bytes ? b.bytes : 16, g->d.device, (void*)g->stream, g_alloc_ctx);
+  // free with the allocator that allocated it, even if the hook changed since
+  if (b.freefn) b.freefn(b.p, b.bytes ? b.bytes : 16, g->d.device, (void*)g->stream, b.ctx);
   else cudaFreeAsync(b.p, g->stream);
   b.p = nullptr;
   b.bytes = 0;
 }
 
 // per-op kernel accounting: launch counts always, CUDA-event device times when g_timing
-enum { K_P1C = 0, K_P1W = 1, K_LEV = 2, K_P2 = 3, K_COMPACT = 4, K_SCAN = 5, K_OTHER = 6 };
+enum { K_P1 = 0, K_P1LIST = 1, K_LEV = 2, K_P2 = 3, K_COMPACT = 4, K_SCAN = 5, K_OTHER = 6 };
 struct Prof {
   cudaStream_t st = nullptr;
   dexel_stats* s = nullptr;
@@ -212,13 +217,12 @@ dexel_status check_radius(float r, double s, int* R) {
 }
 
 // ---------------------------------------------------------------- pass 1
-template <bool WRITE>
-void launch_pass1(int NW, const SrcRows& src, int R, int complement, int row0, int nrows_out, uint32_t* cnt,
-                  const uint64_t* moff, float2* mz, uint8_t* mk, cudaStream_t st) {
-  const int64_t warps = (int64_t)nrows_out * ((src.nx + 31) / 32);
+void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int nrows_out, const PieceSlots& P,
+               int64_t nlist, cudaStream_t st) {
+  const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) pass1_kernel<NWV, WRITE><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, cnt, moff, mz, mk)
+#define P1(NWV) p1_kernel<NWV><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist)
   if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);
@@ -227,33 +231,71 @@ void launch_pass1(int NW, const SrcRows& src, int R, int complement, int row0, i
 #undef P1
 }
 
-struct Pieces {
-  uint64_t* moff = nullptr;
-  float2* mz = nullptr;
-  uint8_t* mk = nullptr;
-  uint64_t m = 0;
-};
-
-dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows_out,
-                       Pieces* P) {
-  const int64_t ncol = (int64_t)nrows_out * src.nx;
+// Pass 1 over rows [row0, row0+nrows) of src: pieces into per-column slots (one launch);
+// columns with more than cap pieces are recomputed into an arena sized from the longest
+// column (a second, tile-list launch); too many of them doubles cap and reruns.
+dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
+                       PieceSlots* P, uint64_t* n_mid) {
+  const int64_t ncol = (int64_t)nrows * src.nx;
+  const int ntiles = (src.nx + 31) / 32;
   const int NW = (32 + 2 * R + 31) / 32;
-  uint32_t* cnt = nullptr;
   dexel_status s;
-  if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&cnt))) return s;
-  if ((s = T.get(sizeof(uint64_t) * (ncol + 1), (void**)&P->moff))) return s;
-  LAUNCH(T, K_P1C, launch_pass1<false>(NW, src, R, complement, row0, nrows_out, cnt, nullptr, nullptr, nullptr, g->stream));
-  CK(cudaGetLastError());
-  if ((s = scan_counts(g, T, cnt, (uint64_t)ncol, P->moff, &P->m))) return s;
-  T.release(cnt);
-  if ((s = T.get(sizeof(float2) * (P->m + 1), (void**)&P->mz))) return s;
-  if ((s = T.get(P->m + 16, (void**)&P->mk))) return s;
-  LAUNCH(T, K_P1W, launch_pass1<true>(NW, src, R, complement, row0, nrows_out, nullptr, P->moff, P->mz, P->mk, g->stream));
-  CK(cudaGetLastError());
-  return DEXEL_OK;
+  *P = PieceSlots{};
+  P->nx = src.nx;
+  P->nrows = nrows;
+  P->cap = g->p1_cap > 0 ? g->p1_cap : 256;
+  P->ovf_list_cap = (unsigned)std::max<int64_t>(256, ncol / 64);
+  if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&P->cnt))) return s;
+  if ((s = T.get(sizeof(int32_t) * (ncol + 1), (void**)&P->ovf_idx))) return s;
+  if ((s = T.get(64, (void**)&P->flags))) return s;
+  P->total = (unsigned long long*)(P->flags + 8);
+  if ((s = T.get(sizeof(uint32_t) * P->ovf_list_cap * 2, (void**)&P->ovf_list))) return s;
+  P->tile_list = P->ovf_list + P->ovf_list_cap;
+  if ((s = T.get(sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), (void**)&P->tile_flag))) return s;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const size_t nslot = (size_t)ncol * (P->cap + 1);
+    if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&P->z))) return s;
+    if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
+    CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
+    CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
+    T.prof.pre(K_P1);
+    launch_p1(NW, src, R, complement, row0, nrows, *P, -1, g->stream);
+    T.prof.post();
+    CK(cudaGetLastError());
+    unsigned hf[3];
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(hf, P->flags, sizeof(hf), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaMemcpyAsync(&tot, P->total, sizeof(tot), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
+      T.release(P->z);
+      T.release(P->k);
+      P->cap *= 2;
+      g->p1_cap = P->cap;
+      continue;
+    }
+    *n_mid += tot;
+    if (hf[0] > 0) {
+      P->ovf_cap = (int)hf[1];
+      const size_t na = (size_t)hf[0] * P->ovf_cap;
+      if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
+      if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
+      T.prof.pre(K_P1LIST);
+      launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], g->stream);
+      T.prof.post();
+      CK(cudaGetLastError());
+    }
+    return DEXEL_OK;
+  }
+  return fail(DEXEL_ECUDA, "pass-1 slot sizing did not converge");
 }
 
-// ---------------------------------------------------------------- levels
+void release_pieces(Temps& T, PieceSlots& P) {
+  for (void* p : {(void*)P.z, (void*)P.k, (void*)P.cnt, (void*)P.ovf_idx, (void*)P.flags, (void*)P.ovf_list,
+                  (void*)P.tile_flag, (void*)P.ovf_z, (void*)P.ovf_k})
+    if (p) T.release(p);
+}
+
 // h(kappa,k) = sqrt(r^2 - (kappa^2 + k^2) s^2) computed in fp64 on the host and rounded once
 // to fp32 (readings R10, R20), -1 where kappa^2 + k^2 > (r/s)^2: the device never
 // evaluates a square root of a weight, and which (kappa, k) contribute is decided exactly.
@@ -280,9 +322,8 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out) {
 dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, int complement,
                         int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev) {
   dexel_status s;
-  Pieces P;
-  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P))) return s;
-  *n_mid += P.m;
+  PieceSlots P;
+  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid))) return s;
   const int64_t ncol = (int64_t)lrn * src.nx;
   unsigned* flags = nullptr;
   if ((s = T.get(64, (void**)&flags))) return s;
@@ -325,7 +366,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
       return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
     if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
     CK(cudaMemsetAsync(flags, 0, 64, g->stream));
-    LvArgs A{P.moff, P.mz, P.mk, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, ovf_list, ovf_cap, nullptr, 0};
+    LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, ovf_list, ovf_cap, nullptr, 0};
     launch(A, ncol);
     CK(cudaGetLastError());
     unsigned hf[2];
@@ -355,9 +396,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     g->lev_cap = L->cap;
     if (attempt == 5) return fail(DEXEL_ECUDA, "level capacity sizing did not converge");
   }
-  T.release(P.mz);
-  T.release(P.mk);
-  T.release(P.moff);
+  release_pieces(T, P);
   T.release(ovf_list);
   T.release(flags);
   return DEXEL_OK;
@@ -488,7 +527,9 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   const int nx = src->d.nx;
   const int nfam = op == OP_SHELL ? 2 : 1;
   int lcap = src->lev_cap > 0 ? src->lev_cap : 8;
-  size_t row_bytes = 0;   // level-slot bytes per level row, all families
+  // bytes per level row of a band: level slots of all families + one family's piece slots
+  const int pcap = src->p1_cap > 0 ? src->p1_cap : 256;
+  size_t row_bytes = (size_t)nx * ((size_t)(pcap + 1) * (sizeof(float2) + 1) + 8);
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
     row_bytes += (size_t)nx * 2 * ((Rf + 1) + (Rf + 2) * sizeof(float2) * (size_t)lcap);
@@ -630,6 +671,7 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
   // initial capacity hints (testing / tuning overrides; grown automatically on overflow)
   if (const char* e = std::getenv("DEXEL_LEV_CAP")) g->lev_cap = std::max(1, std::min(255, std::atoi(e)));
   if (const char* e = std::getenv("DEXEL_P2_ACC")) g->p2_acc = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("DEXEL_P1_CAP")) g->p1_cap = std::max(1, std::atoi(e));
   g->nrows = d->y1 - d->y0;
   g->ncol = (int64_t)g->nrows * d->nx;
   if (d->stream) {
@@ -824,16 +866,29 @@ dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offset
   CK(cudaSetDevice(g->d.device));
   Temps T(g);
   SrcRows rows{(const uint64_t*)g->off.p, (const float*)g->ep.p, g->d.nx, g->nrows, g->d.z_lo, g->d.z_hi};
-  Pieces P;
-  if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, &P))) return s;
-  *n_pieces = P.m;
-  if (cap < P.m) return fail(DEXEL_EOVERFLOW, "capacity < pieces");
-  if (!offsets || (P.m && (!z || !kappa))) return fail(DEXEL_EINVAL, "NULL output buffer");
+  PieceSlots P;
+  uint64_t m = 0;
+  if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, &P, &m))) return s;
+  *n_pieces = m;
+  if (cap < m) return fail(DEXEL_EOVERFLOW, "capacity < pieces");
+  if (!offsets || (m && (!z || !kappa))) return fail(DEXEL_EINVAL, "NULL output buffer");
+  // slots -> CSR on the device (count scan + gather)
+  uint64_t* off = nullptr;
+  float2* oz = nullptr;
+  uint8_t* ok = nullptr;
+  if ((s = T.get(sizeof(uint64_t) * (g->ncol + 1), (void**)&off))) return s;
+  if ((s = T.get(sizeof(float2) * (m + 1), (void**)&oz))) return s;
+  if ((s = T.get(m + 16, (void**)&ok))) return s;
+  uint64_t m2 = 0;
+  if ((s = scan_counts(g, T, P.cnt, (uint64_t)g->ncol, off, &m2))) return s;
+  if (g->ncol > 0)
+    pieces_to_csr<<<(unsigned)((g->ncol + 255) / 256), 256, 0, g->stream>>>(P, g->ncol, off, oz, ok);
+  CK(cudaGetLastError());
   const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpyAsync(offsets, P.moff, sizeof(uint64_t) * (g->ncol + 1), k, g->stream));
-  if (P.m) {
-    CK(cudaMemcpyAsync(z, P.mz, sizeof(float2) * P.m, k, g->stream));
-    CK(cudaMemcpyAsync(kappa, P.mk, P.m, k, g->stream));
+  CK(cudaMemcpyAsync(offsets, off, sizeof(uint64_t) * (g->ncol + 1), k, g->stream));
+  if (m) {
+    CK(cudaMemcpyAsync(z, oz, sizeof(float2) * m, k, g->stream));
+    CK(cudaMemcpyAsync(kappa, ok, m, k, g->stream));
   }
   CK(cudaStreamSynchronize(g->stream));
   return DEXEL_OK;

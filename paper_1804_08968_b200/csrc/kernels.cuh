@@ -1,15 +1,15 @@
 // kernels.cuh -- sm_100a kernels of the separable dexel offset (arXiv 1804.08968).
 //
 //   validate_kernel   upload check (strictly increasing, finite, in domain)
-//   pass1_kernel      pass 1 along x: closest-parent extrusion S_In -> S_Mid
+//   p1_kernel         pass 1 along x: closest-parent extrusion S_In -> S_Mid
 //                     (PAPER.md:494-501).  One warp per 32 output columns of a
 //                     row; the warp sweeps z over the window's endpoints (merged
 //                     across lanes with a REDUX min on order-preserving keys), keeps
 //                     the active neighbour columns as a ballot bitmask and each lane
 //                     reads its closest parent kappa = nearest set bit within R.
 // The z-resolution (levels.cuh) and pass 2 (pass2.cuh) live in their own headers.
-// pass1 runs twice (two-phase allocation): COUNT writes per-column counts, WRITE
-// recomputes and writes at the scanned offsets.
+// Pass 1 runs once per band: pieces go to per-column slots, the rare columns that
+// outgrow them are recomputed into an arena by a second, list-driven launch.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -117,27 +117,58 @@ __device__ __forceinline__ int nearest_parent<2>(const uint32_t (&M)[2], int p, 
   return d <= R ? d : KNONE;
 }
 
+// Pass-1 output: the pieces of every column of a band of rows in per-column slots.
+// Slot-major: piece t of column (row, i) at z[(row*(cap+1) + t)*nx + i] -- a warp of 32
+// consecutive columns reads (levels kernel) 256 contiguous bytes per slot.  Slot `cap` is a
+// spill cell: writes beyond cap are clamped there, the column is listed, and a second
+// launch ("list mode") rewrites the listed columns' pieces into an arena of ovf_cap pieces
+// per column.
+struct PieceSlots {
+  float2* z;           // [nrows][cap+1][nx]  (lo, hi)
+  uint8_t* k;          // [nrows][cap+1][nx]  kappa
+  uint32_t* cnt;       // [nrows*nx]          true piece count
+  int cap, nx, nrows;
+  int32_t* ovf_idx;    // [nrows*nx] arena slot of an overflow column (valid where cnt > cap)
+  float2* ovf_z;       // [n_ovf][ovf_cap]
+  uint8_t* ovf_k;
+  int ovf_cap;
+  uint32_t* ovf_list;  // overflow columns (main pass appends)
+  unsigned ovf_list_cap;
+  uint32_t* tile_flag; // [nrows * ntiles] a tile holds an overflow column
+  uint32_t* tile_list; // tiles to rerun in list mode
+  unsigned* flags;     // [0] overflow columns, [1] longest column (when > cap), [2] tiles listed
+  unsigned long long* total;   // pieces (statistics)
+};
+
+__host__ __device__ __forceinline__ size_t piece_index(const PieceSlots& P, int row, int t, int i) {
+  return ((size_t)row * (P.cap + 1) + t) * P.nx + i;
+}
+
 // One warp = output columns [32*tile, 32*tile+32) of output row jr (source row j = row0 + jr).
 // NW = number of 32-bit words of the window mask (window = 32 + 2R columns).
-// The window's endpoints (S, or its complement within [z_lo, z_hi], as
-// order-preserving u32 keys) are first staged in shared memory -- one
-// contiguous copy per window column -- so the sweep loop touches no global
-// memory; windows larger than the staging area fall back to __ldg reads.
+// The window's endpoints (S, or its complement within [z_lo, z_hi], as order-preserving
+// u32 keys) are first staged in shared memory -- one contiguous copy per window column --
+// so the sweep touches no global memory (windows larger than the staging area read
+// through __ldg).  Each step of the sweep takes the next z over the whole window with one
+// REDUX min, toggles the window's activity mask with one ballot per word (a column's
+// events alternate start / end), and every lane reads its closest parent
+// kappa = min |dx| as the nearest set bit within R of its own position.
+// Pure selection: lo / hi are copies of input values, kappa an integer.
 constexpr int P1_WARPS = 4;
 constexpr int P1_STAGE = 2048;   // keys per warp (8 KB)
 
-template <int NW, bool WRITE>
-__global__ void __launch_bounds__(P1_WARPS * 32) pass1_kernel(SrcRows src, int R, int complement, int row0,
-                                                               int nrows_out, uint32_t* __restrict__ cnt,
-                                                               const uint64_t* __restrict__ moff,
-                                                               float2* __restrict__ mz, uint8_t* __restrict__ mk) {
+template <int NW>
+__global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, int complement, int row0,
+                                                            int nrows_out, PieceSlots P, int64_t nlist) {
   __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
   const int lane = threadIdx.x & 31;
   uint32_t* stage = stage_all[threadIdx.x >> 5];
   const int ntiles = (src.nx + 31) >> 5;
+  const bool list_mode = nlist >= 0;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= (int64_t)nrows_out * ntiles) return;  // warp-uniform
-  const int jr = (int)(gw / ntiles), tile = (int)(gw % ntiles);
+  if (gw >= (list_mode ? nlist : (int64_t)nrows_out * ntiles)) return;  // warp-uniform
+  const int64_t tl = list_mode ? (int64_t)P.tile_list[gw] : gw;
+  const int jr = (int)(tl / ntiles), tile = (int)(tl % ntiles);
   const int j = row0 + jr;
   const int i0 = tile * 32;
   const int W = 32 + 2 * R;
@@ -161,36 +192,51 @@ __global__ void __launch_bounds__(P1_WARPS * 32) pass1_kernel(SrcRows src, int R
     total += __shfl_sync(FULL, incl, 31);
   }
   const bool staged = total <= (uint32_t)P1_STAGE;
-  if (staged) {
 #pragma unroll
-    for (int q = 0; q < NW; ++q) {
-      const uint32_t nv = cur[q].vend - cur[q].v;
+  for (int q = 0; q < NW; ++q) {
+    const uint32_t nv = cur[q].vend - cur[q].v;
+    if (staged) {
       for (uint32_t t = 0; t < nv; ++t) stage[sb[q] + t] = fkey(col_value(src, cur[q], cur[q].v + t, complement));
       pos[q] = sb[q];
       end[q] = sb[q] + nv;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < NW; ++q) nkey[q] = pos[q] < end[q] ? stage[pos[q]] : KEY_NONE;
-  } else {
-#pragma unroll
-    for (int q = 0; q < NW; ++q) {
+    } else {
       pos[q] = cur[q].v;
       end[q] = cur[q].vend;
-      nkey[q] = pos[q] < end[q] ? fkey(col_value(src, cur[q], pos[q], complement)) : KEY_NONE;
     }
   }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < NW; ++q)
+    nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(col_value(src, cur[q], pos[q], complement)))
+                              : KEY_NONE;
 
   const int i = i0 + lane;
   const bool out_ok = i < src.nx;
   const int64_t c = (int64_t)jr * src.nx + i;
-  uint64_t wbase = 0;
-  if (WRITE && out_ok) wbase = moff[c];
-  uint32_t npieces = 0;
-  uint32_t act = 0;
+  // where this lane's pieces go: slots (main pass), the arena (list mode, overflow columns), nowhere
+  float2* zb = nullptr;
+  uint8_t* kb = nullptr;
+  uint32_t zstep = 0, tmax = 0;
+  if (out_ok) {
+    if (!list_mode) {
+      zb = P.z + piece_index(P, jr, 0, i);
+      kb = P.k + piece_index(P, jr, 0, i);
+      zstep = (uint32_t)P.nx;
+      tmax = (uint32_t)P.cap;                      // spill cell
+    } else if (P.cnt[c] > (uint32_t)P.cap) {
+      const size_t q = (size_t)P.ovf_idx[c] * P.ovf_cap;
+      zb = P.ovf_z + q;
+      kb = P.ovf_k + q;
+      zstep = 1;
+      tmax = (uint32_t)P.ovf_cap - 1;
+    }
+  }
+  uint32_t M[NW];
+#pragma unroll
+  for (int q = 0; q < NW; ++q) M[q] = 0u;          // window activity mask (warp-uniform)
+  uint32_t np = 0;
   int kap = KNONE;
   float zstart = 0.f;
-
   for (;;) {
     uint32_t my = KEY_NONE;
 #pragma unroll
@@ -199,33 +245,68 @@ __global__ void __launch_bounds__(P1_WARPS * 32) pass1_kernel(SrcRows src, int R
     if (zk == KEY_NONE) break;
 #pragma unroll
     for (int q = 0; q < NW; ++q) {
-      if (nkey[q] == zk) {
-        // virtual index parity: even = interval start (cur.v is even)
-        const uint32_t rel = pos[q] - (staged ? sb[q] : 0u) + (staged ? cur[q].v : 0u);
-        act = (rel & 1u) == 0u ? (act | (1u << q)) : (act & ~(1u << q));
+      const bool hit = nkey[q] == zk;
+      M[q] ^= __ballot_sync(FULL, hit);
+      if (hit) {
         ++pos[q];
         nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(col_value(src, cur[q], pos[q], complement)))
                                   : KEY_NONE;
       }
     }
-    uint32_t M[NW];
-#pragma unroll
-    for (int t = 0; t < NW; ++t) M[t] = __ballot_sync(FULL, (act >> t) & 1u);
     const int knew = nearest_parent<NW>(M, lane + R, R);
     if (knew != kap) {
       const float z = keyf(zk);
-      if (kap != KNONE && out_ok) {
-        if (WRITE) {
-          mz[wbase + npieces] = make_float2(zstart, z);
-          mk[wbase + npieces] = (uint8_t)kap;
+      if (kap != KNONE) {
+        if (zb) {
+          const uint32_t t = min(np, tmax);
+          zb[(size_t)t * zstep] = make_float2(zstart, z);
+          kb[(size_t)t * zstep] = (uint8_t)kap;
         }
-        ++npieces;
+        ++np;
       }
       kap = knew;
       zstart = z;
     }
   }
-  if (!WRITE && out_ok) cnt[c] = npieces;
+  if (!list_mode) {
+    if (out_ok) {
+      P.cnt[c] = np;
+      if (np > (uint32_t)P.cap) {                    // hand the column to list mode
+        atomicMax(P.flags + 1, np);
+        const unsigned slot = atomicAdd(P.flags, 1u);
+        if (slot < P.ovf_list_cap) {
+          P.ovf_idx[c] = (int32_t)slot;
+          const size_t tf = (size_t)jr * ntiles + tile;
+          if (atomicExch(P.tile_flag + tf, 1u) == 0u) {
+            const unsigned ts = atomicAdd(P.flags + 2, 1u);
+            P.tile_list[ts] = (uint32_t)tf;
+          }
+        }
+      }
+    }
+    const unsigned wsum = __reduce_add_sync(FULL, out_ok ? np : 0u);
+    if (lane == 0 && wsum) atomicAdd(P.total, (unsigned long long)wsum);
+  }
+}
+
+// pieces of a band (slots + arena) -> CSR (dexel_pass1, parity testing only)
+__global__ void pieces_to_csr(PieceSlots P, int64_t ncol, const uint64_t* __restrict__ off, float2* __restrict__ oz,
+                              uint8_t* __restrict__ ok) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncol) return;
+  const int row = (int)(c / P.nx), i = (int)(c % P.nx);
+  const uint32_t m = P.cnt[c];
+  const uint64_t o = off[c];
+  for (uint32_t t = 0; t < m; ++t) {
+    if (m <= (uint32_t)P.cap) {
+      oz[o + t] = P.z[piece_index(P, row, (int)t, i)];
+      ok[o + t] = P.k[piece_index(P, row, (int)t, i)];
+    } else {
+      const size_t q = (size_t)P.ovf_idx[c] * P.ovf_cap + t;
+      oz[o + t] = P.ovf_z[q];
+      ok[o + t] = P.ovf_k[q];
+    }
+  }
 }
 
 }  // namespace dexel

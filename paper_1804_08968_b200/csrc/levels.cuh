@@ -38,6 +38,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "kernels.cuh"
+
 namespace dexel {
 
 constexpr int LV_OVF_CAP = 255;   // list capacity in the overflow arena (counts are u8)
@@ -69,9 +71,7 @@ __host__ __device__ __forceinline__ size_t ovf_z_index(const LevelSlots& L, int 
 }
 
 struct LvArgs {
-  const uint64_t* moff;    // pieces CSR offsets [ncol+1] (columns of the level rows)
-  const float2* mz;        // (lo, hi)
-  const uint8_t* mk;       // kappa
+  PieceSlots P;            // pass-1 pieces of the level rows (kernels.cuh)
   int64_t ncol;
   const float* h;          // [(R+1)^2] fl32(sqrt(r^2 - (kappa^2 + k^2) s^2)), -1 where negative
   float zlo, zhi;
@@ -116,8 +116,21 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     const int64_t c = A.list ? (int64_t)A.list[g] : g;
     const int q = A.list ? (int)g : -1;
     const int row = (int)(c / A.L.nx), i = (int)(c % A.L.nx);
-    const uint64_t base = A.moff[c];
-    const int m = (int)(A.moff[c + 1] - base);
+    // this column's pieces: slots (stride nx, coalesced across the warp) or the overflow arena
+    const int m = (int)A.P.cnt[c];
+    const float2* zc;
+    const uint8_t* kc;
+    int64_t ps;
+    if (m <= A.P.cap) {
+      zc = A.P.z + piece_index(A.P, row, 0, i);
+      kc = A.P.k + piece_index(A.P, row, 0, i);
+      ps = A.P.nx;
+    } else {
+      const size_t qo = (size_t)A.P.ovf_idx[c] * A.P.ovf_cap;
+      zc = A.P.ovf_z + qo;
+      kc = A.P.ovf_k + qo;
+      ps = 1;
+    }
     float a[LMAX], b[LMAX];
     uint32_t o[LMAX];   // next slot of level k0+k, as a float2 offset from slot 0 / level k0 of the block
     const uint32_t nx = (uint32_t)A.L.nx, S = (uint32_t)(R + 2) * nx;      // S = one slot (all levels)
@@ -143,17 +156,17 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     if (ok_) Zd[min(o[k], olim)] = make_float2(a[k], b[k]);                   \
     o[k] += ok_ ? ostep : 0u;                                                 \
   }
-      float2 nz = m > 0 ? A.mz[base + (d ? m - 1 : 0)] : make_float2(0.f, 0.f);
-      int nk = m > 0 ? A.mk[base + (d ? m - 1 : 0)] : 0;
-      float2 nz2 = m > 1 ? A.mz[base + (d ? m - 2 : 1)] : make_float2(0.f, 0.f);
-      int nk2 = m > 1 ? A.mk[base + (d ? m - 2 : 1)] : 0;
+      float2 nz = m > 0 ? zc[(d ? m - 1 : 0) * ps] : make_float2(0.f, 0.f);
+      int nk = m > 0 ? kc[(d ? m - 1 : 0) * ps] : 0;
+      float2 nz2 = m > 1 ? zc[(d ? m - 2 : 1) * ps] : make_float2(0.f, 0.f);
+      int nk2 = m > 1 ? kc[(d ? m - 2 : 1) * ps] : 0;
       for (int t = 0; t < m; ++t) {
         const float2 p = nz;
         const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
         nz = nz2; nk = nk2;
         if (t + 2 < m) {
-          const uint64_t idx = base + (d ? (uint64_t)(m - 3 - t) : (uint64_t)(t + 2));
-          nz2 = A.mz[idx]; nk2 = A.mk[idx];
+          const int64_t idx = (d ? (int64_t)(m - 3 - t) : (int64_t)(t + 2)) * ps;
+          nz2 = zc[idx]; nk2 = kc[idx];
         }
         float hv[4 * NV];
 #pragma unroll

@@ -241,8 +241,8 @@ def test_torch_allocator_hook(dx):
 
 
 
-@pytest.mark.parametrize("lev_cap,acc,band", [("1", "1", "3"), ("2", "4", "7")])
-def test_capacity_regrowth(dx, lev_cap, acc, band):
+@pytest.mark.parametrize("lev_cap,acc,band,p1cap", [("1", "1", "3", "1"), ("2", "4", "7", "6")])
+def test_capacity_regrowth(dx, lev_cap, acc, band, p1cap):
     """Start every capacity at its minimum (level slots per list, pass-2 accumulator:
     DEXEL_LEV_CAP / DEXEL_P2_ACC) so every op overflows and reruns with grown
     capacities, and cut the grid into 3-row bands (DEXEL_BAND_ROWS); results still
@@ -268,7 +268,7 @@ for seed in range(12):
         res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (op, r, res)
 print("OK")
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DEXEL_LEV_CAP=lev_cap, DEXEL_P2_ACC=acc, DEXEL_BAND_ROWS=band)
+    env = dict(os.environ, DEXEL_LEV_CAP=lev_cap, DEXEL_P2_ACC=acc, DEXEL_BAND_ROWS=band, DEXEL_P1_CAP=p1cap)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
 
@@ -299,3 +299,30 @@ def test_pass1_bitwise_unstaged_windows(dx):
             ref = O.pass1(host, r, complement=comp)
             assert np.array_equal(off, ref.off) and np.array_equal(z.astype(np.float64), ref.z) \
                 and np.array_equal(k, ref.k)
+
+
+def test_pass1_bitwise_overflow_arena(dx):
+    """Pass-1 pieces of columns that outgrow their slots (DEXEL_P1_CAP=2) come from the
+    overflow arena (second, tile-list launch); still bitwise equal to the oracle's P1."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
+for seed in range(10):
+    rs = np.random.default_rng(900 + seed)
+    host = G.random_grid(int(rs.integers(20, 70)), int(rs.integers(2, 9)), 5, -10.0, 10.0, seed,
+                         quantum=0.25 if seed %% 2 else None)
+    r = float(rs.choice([1.0, 3.0, 6.5, 20.0]))
+    src = dx.Grid.from_host(host)
+    for comp in (False, True):
+        off, z, k = dx.dexel_pass1(src, r, comp)
+        ref = O.pass1(host, r, complement=comp)
+        assert np.array_equal(off, ref.off) and np.array_equal(z.astype(np.float64), ref.z) \
+            and np.array_equal(k, ref.k), (seed, r, comp)
+print("OK")
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DEXEL_P1_CAP="2")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
