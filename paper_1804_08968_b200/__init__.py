@@ -58,6 +58,7 @@ ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctyp
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
 
 _lib = None
+_alloc_keep = []   # every allocator callback pair ever installed (kept alive)
 
 
 def lib():
@@ -119,8 +120,9 @@ def use_torch_allocator(enable: bool = True):
     global _alloc_refs
     L = lib()
     if not enable:
+        # the callbacks stay referenced (module-level list): buffers allocated through them
+        # are still released through them by the library
         _check(L.dexel_set_allocator(ALLOC_FN(), FREE_FN(), None))
-        _alloc_refs = None
         return
     import torch
 
@@ -134,6 +136,7 @@ def use_torch_allocator(enable: bool = True):
         torch.cuda.caching_allocator_delete(ptr)
 
     _alloc_refs = (ALLOC_FN(_alloc), FREE_FN(_free))
+    _alloc_keep.append(_alloc_refs)
     _check(L.dexel_set_allocator(_alloc_refs[0], _alloc_refs[1], None))
 
 
