@@ -218,11 +218,11 @@ dexel_status check_radius(float r, double s, int* R) {
 
 // ---------------------------------------------------------------- pass 1
 void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int nrows_out, const PieceSlots& P,
-               int64_t nlist, cudaStream_t st) {
+               int64_t nlist, const float* prune, cudaStream_t st) {
   const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) p1_kernel<NWV><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist)
+#define P1(NWV) p1_kernel<NWV><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
   if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);
@@ -235,7 +235,7 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
 // columns with more than cap pieces are recomputed into an arena sized from the longest
 // column (a second, tile-list launch); too many of them doubles cap and reruns.
 dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
-                       PieceSlots* P, uint64_t* n_mid) {
+                       PieceSlots* P, uint64_t* n_mid, const float* prune) {
   const int64_t ncol = (int64_t)nrows * src.nx;
   const int ntiles = (src.nx + 31) / 32;
   const int NW = (32 + 2 * R + 31) / 32;
@@ -258,8 +258,9 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
     if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
     CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
     CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
+    CK(cudaMemsetAsync(P->ovf_idx, 0xff, sizeof(int32_t) * (ncol + 1), g->stream));   // -1: slots
     T.prof.pre(K_P1);
-    launch_p1(NW, src, R, complement, row0, nrows, *P, -1, g->stream);
+    launch_p1(NW, src, R, complement, row0, nrows, *P, -1, prune, g->stream);
     T.prof.post();
     CK(cudaGetLastError());
     unsigned hf[3];
@@ -274,17 +275,20 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
       g->p1_cap = P->cap;
       continue;
     }
-    *n_mid += tot;
     if (hf[0] > 0) {
       P->ovf_cap = (int)hf[1];
       const size_t na = (size_t)hf[0] * P->ovf_cap;
       if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
       if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
       T.prof.pre(K_P1LIST);
-      launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], g->stream);
+      launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], prune, g->stream);
       T.prof.post();
       CK(cudaGetLastError());
+      // the list launch adds the arena columns' (filtered) counts to the total
+      CK(cudaMemcpyAsync(&tot, P->total, sizeof(tot), cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
     }
+    *n_mid += tot;
     return DEXEL_OK;
   }
   return fail(DEXEL_ECUDA, "pass-1 slot sizing did not converge");
@@ -299,7 +303,7 @@ void release_pieces(Temps& T, PieceSlots& P) {
 // h(kappa,k) = sqrt(r^2 - (kappa^2 + k^2) s^2) computed in fp64 on the host and rounded once
 // to fp32 (readings R10, R20), -1 where kappa^2 + k^2 > (r/s)^2: the device never
 // evaluates a square root of a weight, and which (kappa, k) contribute is decided exactly.
-dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out) {
+dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, float** prune) {
   const double s = g->d.spacing;
   const int n1 = R + 1;
   std::vector<float> h((size_t)n1 * n1);
@@ -309,21 +313,29 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out) {
       const double w = rr - ((double)a * a + (double)k * k) * s * s;   // exact for fp32 r, small integers
       h[(size_t)a * n1 + k] = w >= 0.0 ? (float)std::sqrt(w) : -1.0f;
     }
+  // capsule-domination table for the pass-1 filter: h(kappa, 0), rounded once to fp32
+  // (DEXEL_NO_PRUNE=1 disables the filter)
+  std::vector<float> h0(n1);
+  for (int a = 0; a < n1; ++a) h0[a] = (float)std::sqrt(std::max(0.0, rr - (double)a * a * s * s));
   dexel_status st;
-  if ((st = T.get(sizeof(float) * h.size() + 16, (void**)out))) return st;
+  if ((st = T.get(sizeof(float) * (h.size() + n1) + 16, (void**)out))) return st;
+  float* d0 = *out + h.size();
   CK(cudaMemcpyAsync(*out, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
-  CK(cudaStreamSynchronize(g->stream));  // the host vector goes out of scope
+  CK(cudaMemcpyAsync(d0, h0.data(), sizeof(float) * n1, cudaMemcpyHostToDevice, g->stream));
+  CK(cudaStreamSynchronize(g->stream));  // the host vectors go out of scope
+  const char* e = std::getenv("DEXEL_NO_PRUNE");
+  *prune = (e && std::atoi(e)) ? nullptr : d0;
   return DEXEL_OK;
 }
 
 // level slots of one family for level rows [lr0, lr0 + lrn) (extended-row numbering):
 // pass 1 on those rows, then the level-set kernel; the pieces are freed on return.
 // A level list longer than the slot capacity reruns the level kernel with a larger cap.
-dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, int complement,
-                        int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev) {
+dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, const float* prune,
+                        int complement, int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev) {
   dexel_status s;
   PieceSlots P;
-  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid))) return s;
+  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid, prune))) return s;
   const int64_t ncol = (int64_t)lrn * src.nx;
   unsigned* flags = nullptr;
   if ((s = T.get(64, (void**)&flags))) return s;
@@ -520,8 +532,10 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   // h(kappa, k) tables, one per family radius
   float* htab_a = nullptr;
   float* htab_b = nullptr;
-  if ((s = make_htab(src, T, r_a, Ra, &htab_a))) return s;
-  if (op == OP_SHELL && (s = make_htab(src, T, r_b, Rb, &htab_b))) return s;
+  float* prune_a = nullptr;
+  float* prune_b = nullptr;
+  if ((s = make_htab(src, T, r_a, Ra, &htab_a, &prune_a))) return s;
+  if (op == OP_SHELL && (s = make_htab(src, T, r_b, Rb, &htab_b, &prune_b))) return s;
   // ---- row bands: level slots of (band + R-row halo) rows, then pass 2 of the band
   const int64_t ncol = src->ncol;
   const int nx = src->d.nx;
@@ -559,13 +573,13 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
       const int lr0 = std::max(0, hlo + b0 - Rmax), lr1 = std::min(nrows_ext, hlo + b1 + Rmax);
       LevelSlots LA{}, LB{};
       // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
-      if ((s = run_levels(src, T, rows, Ra, htab_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
+      if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
                           &stats.n_lev))) {
         set_empty(dst);
         return s;
       }
       if (op == OP_SHELL) {
-        if ((s = run_levels(src, T, rows, Rb, htab_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev))) {
+        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev))) {
           set_empty(dst);
           return s;
         }
@@ -868,7 +882,8 @@ dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offset
   SrcRows rows{(const uint64_t*)g->off.p, (const float*)g->ep.p, g->d.nx, g->nrows, g->d.z_lo, g->d.z_hi};
   PieceSlots P;
   uint64_t m = 0;
-  if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, &P, &m))) return s;
+  // unfiltered pieces (no capsule-domination pruning): bitwise comparable with the oracle's P1
+  if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, &P, &m, nullptr))) return s;
   *n_pieces = m;
   if (cap < m) return fail(DEXEL_EOVERFLOW, "capacity < pieces");
   if (!offsets || (m && (!z || !kappa))) return fail(DEXEL_EINVAL, "NULL output buffer");

@@ -128,7 +128,7 @@ struct PieceSlots {
   uint8_t* k;          // [nrows][cap+1][nx]  kappa
   uint32_t* cnt;       // [nrows*nx]          true piece count
   int cap, nx, nrows;
-  int32_t* ovf_idx;    // [nrows*nx] arena slot of an overflow column (valid where cnt > cap)
+  int32_t* ovf_idx;    // [nrows*nx] arena slot of an overflow column, -1 elsewhere
   float2* ovf_z;       // [n_ovf][ovf_cap]
   uint8_t* ovf_k;
   int ovf_cap;
@@ -157,10 +157,31 @@ __host__ __device__ __forceinline__ size_t piece_index(const PieceSlots& P, int 
 constexpr int P1_WARPS = 4;
 constexpr int P1_STAGE = 2048;   // keys per warp (8 KB)
 
+// Capsule domination (prune != nullptr): piece q dominates piece p when kappa_q <= kappa_p and
+//   max(lo_q - lo_p, hi_p - hi_q) <= h(kappa_q, 0) - h(kappa_p, 0),   h(kappa, k) = sqrt(r^2 - (kappa^2+k^2)s^2):
+// h(kappa_q,k) - h(kappa_p,k) grows with k, so then p's capsule cross-section lies inside q's at
+// every level where p reaches, and dropping p leaves every level set L_k -- hence the result --
+// unchanged (the union of the capsules is all pass 2 needs).  Each lane keeps
+// its last piece pending and tests it against the next one (a dominated staircase step of a
+// sphere is typically shorter than the h difference of its neighbour): about 45% of the pieces
+// of the synthetic configs go.  The next piece n lies above the pending one p, so the two tests
+// reduce to  n dominates p: kn <= kp and lo_n - lo_p <= H[kn] - H[kp];  p dominates n:
+// kp <= kn and hi_n - hi_p <= H[kp] - H[kn]  (H = h(., 0), fp32).  Both sides are differences
+// of nearby values (error ~2^-24 of the result), and a piece is only dropped with a relative
+// margin of 1e-6, so rounding can keep a dominated piece but never drop a needed one.
+__device__ __forceinline__ bool dom_margin(float lhs, float rhs) {
+  return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs));
+}
+
 template <int NW>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, int complement, int row0,
-                                                            int nrows_out, PieceSlots P, int64_t nlist) {
+                                                            int nrows_out, PieceSlots P, int64_t nlist,
+                                                            const float* __restrict__ prune) {
   __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
+  __shared__ float h0[256];
+  if (prune)
+    for (int t = threadIdx.x; t <= R; t += blockDim.x) h0[t] = prune[t];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   uint32_t* stage = stage_all[threadIdx.x >> 5];
   const int ntiles = (src.nx + 31) >> 5;
@@ -223,7 +244,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       kb = P.k + piece_index(P, jr, 0, i);
       zstep = (uint32_t)P.nx;
       tmax = (uint32_t)P.cap;                      // spill cell
-    } else if (P.cnt[c] > (uint32_t)P.cap) {
+    } else if (P.ovf_idx[c] >= 0) {
       const size_t q = (size_t)P.ovf_idx[c] * P.ovf_cap;
       zb = P.ovf_z + q;
       kb = P.ovf_k + q;
@@ -237,6 +258,17 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   uint32_t np = 0;
   int kap = KNONE;
   float zstart = 0.f;
+  // pending piece of the capsule-domination filter
+  float plo = 0.f, phi = 0.f;
+  int pk = KNONE;
+  auto put = [&](float lo, float hi, int k) {
+    if (zb) {
+      const uint32_t t = min(np, tmax);
+      zb[(size_t)t * zstep] = make_float2(lo, hi);
+      kb[(size_t)t * zstep] = (uint8_t)k;
+    }
+    ++np;
+  };
   for (;;) {
     uint32_t my = KEY_NONE;
 #pragma unroll
@@ -257,17 +289,25 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     if (knew != kap) {
       const float z = keyf(zk);
       if (kap != KNONE) {
-        if (zb) {
-          const uint32_t t = min(np, tmax);
-          zb[(size_t)t * zstep] = make_float2(zstart, z);
-          kb[(size_t)t * zstep] = (uint8_t)kap;
+        if (!prune) {
+          put(zstart, z, kap);
+        } else if (pk == KNONE) {
+          plo = zstart; phi = z; pk = kap;
+        } else {
+          const float D = h0[pk] - h0[kap];                    // H[kp] - H[kn]
+          if (pk <= kap && dom_margin(z - phi, D)) {
+            // the pending piece covers the new one
+          } else {
+            if (!(kap <= pk && dom_margin(zstart - plo, -D))) put(plo, phi, pk);
+            plo = zstart; phi = z; pk = kap;
+          }
         }
-        ++np;
       }
       kap = knew;
       zstart = z;
     }
   }
+  if (prune && pk != KNONE) put(plo, phi, pk);
   if (!list_mode) {
     if (out_ok) {
       P.cnt[c] = np;
@@ -284,8 +324,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
         }
       }
     }
-    const unsigned wsum = __reduce_add_sync(FULL, out_ok ? np : 0u);
+    const unsigned wsum = __reduce_add_sync(FULL, (out_ok && np <= (uint32_t)P.cap) ? np : 0u);   // arena: list launch
     if (lane == 0 && wsum) atomicAdd(P.total, (unsigned long long)wsum);
+  } else if (zb) {
+    P.cnt[c] = np;                                   // the filtered count of an arena column
+    atomicAdd(P.total, (unsigned long long)np);
   }
 }
 
@@ -297,8 +340,9 @@ __global__ void pieces_to_csr(PieceSlots P, int64_t ncol, const uint64_t* __rest
   const int row = (int)(c / P.nx), i = (int)(c % P.nx);
   const uint32_t m = P.cnt[c];
   const uint64_t o = off[c];
+  const bool arena = P.ovf_idx[c] >= 0;
   for (uint32_t t = 0; t < m; ++t) {
-    if (m <= (uint32_t)P.cap) {
+    if (!arena) {
       oz[o + t] = P.z[piece_index(P, row, (int)t, i)];
       ok[o + t] = P.k[piece_index(P, row, (int)t, i)];
     } else {

@@ -101,27 +101,34 @@ struct LvTab {
 template <int LMAX>
 __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs A) {
   constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
-  __shared__ __align__(16) float Hs[256 * HS];   // h(kappa, k0 + k), -inf beyond R or out of reach
+  __shared__ __align__(16) float Hs[257 * HS];   // h(kappa, k0 + k), -inf beyond R or out of reach;
+                                                  // row R+1: all -inf (the "null piece")
   const int R = A.L.R, L1 = R + 1;
   const int k0 = blockIdx.y * LMAX;
-  for (int t = threadIdx.x; t < L1 * HS; t += LV_T) {
+  for (int t = threadIdx.x; t < (L1 + 1) * HS; t += LV_T) {
     const int kap = t / HS, kk = t % HS, k = k0 + kk;
-    const float h = (kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
+    const float h = (kap <= R && kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
     Hs[t] = h >= 0.f ? h : -INFINITY;
   }
   __syncthreads();
   uint32_t tot = 0, mx = 0;
   const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
-  if (g < (A.list ? A.nlist : A.ncol)) {
-    const int64_t c = A.list ? (int64_t)A.list[g] : g;
+  const bool live = g < (A.list ? A.nlist : A.ncol);
+  // every lane of the warp walks the same piece index t (0..mmax-1 forward, mmax-1..0 backward):
+  // the slot reads stay coalesced and the loop never diverges; a lane past its own count
+  // processes the "null piece", which leaves both running unions unchanged
+  const int m_live = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
+  const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)m_live);
+  {   // all 32 lanes run the loop (warp-uniform trip count and __all_sync); dead lanes see m = 0
+    const int64_t c = live ? (A.list ? (int64_t)A.list[g] : g) : 0;
     const int q = A.list ? (int)g : -1;
     const int row = (int)(c / A.L.nx), i = (int)(c % A.L.nx);
     // this column's pieces: slots (stride nx, coalesced across the warp) or the overflow arena
-    const int m = (int)A.P.cnt[c];
+    const int m = m_live;
     const float2* zc;
     const uint8_t* kc;
     int64_t ps;
-    if (m <= A.P.cap) {
+    if (m <= A.P.cap) {   // (a column's pieces live in the arena exactly when it has more than cap)
       zc = A.P.z + piece_index(A.P, row, 0, i);
       kc = A.P.k + piece_index(A.P, row, 0, i);
       ps = A.P.nx;
@@ -156,25 +163,30 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     if (ok_) Zd[min(o[k], olim)] = make_float2(a[k], b[k]);                   \
     o[k] += ok_ ? ostep : 0u;                                                 \
   }
-      float2 nz = m > 0 ? zc[(d ? m - 1 : 0) * ps] : make_float2(0.f, 0.f);
-      int nk = m > 0 ? kc[(d ? m - 1 : 0) * ps] : 0;
-      float2 nz2 = m > 1 ? zc[(d ? m - 2 : 1) * ps] : make_float2(0.f, 0.f);
-      int nk2 = m > 1 ? kc[(d ? m - 2 : 1) * ps] : 0;
-      for (int t = 0; t < m; ++t) {
+      // null piece: U_f (-inf, -inf), U_r (+inf, +inf), kappa row R+1 (all -inf)
+      const float2 nullp = d ? make_float2(INFINITY, INFINITY) : make_float2(-INFINITY, -INFINITY);
+      auto fetch = [&](int s, float2& z, int& kk) {
+        const int t = d ? mmax - 1 - s : s;
+        if (s < mmax && t < m) { z = zc[(int64_t)t * ps]; kk = kc[(int64_t)t * ps]; }
+        else { z = nullp; kk = L1; }
+      };
+      float2 nz, nz2;
+      int nk, nk2;
+      fetch(0, nz, nk);
+      fetch(1, nz2, nk2);
+      for (int s = 0; s < mmax; ++s) {
         const float2 p = nz;
         const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
         nz = nz2; nk = nk2;
-        if (t + 2 < m) {
-          const int64_t idx = (d ? (int64_t)(m - 3 - t) : (int64_t)(t + 2)) * ps;
-          nz2 = zc[idx]; nk2 = kc[idx];
-        }
+        fetch(s + 2, nz2, nk2);
         float hv[4 * NV];
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           const float4 v = hrow[j];
           hv[4 * j] = v.x; hv[4 * j + 1] = v.y; hv[4 * j + 2] = v.z; hv[4 * j + 3] = v.w;
         }
-        if (hv[0] == -INFINITY) continue;   // reach is monotone in k: the whole chunk is out of reach
+        // reach is monotone in k: skip when no lane's piece reaches this chunk (warp-uniform)
+        if (__all_sync(0xffffffffu, hv[0] == -INFINITY)) continue;
         if (d == 0) {                        // U_f: forward running union of [lo, hi + h]
 #pragma unroll
           for (int k = 0; k < LMAX; ++k) {
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
       for (int k = 0; k < LMAX; ++k) {
         LV_EMIT(k, true);
 #undef LV_EMIT
-        if (k0 + k <= R) {
+        if (live && k0 + k <= R) {
           const uint32_t nk_ = (o[k] - (uint32_t)k * olev) / ostep;
           if (q < 0) A.L.cnt[slot_cnt_index(A.L, row, d, k0 + k, i)] = (uint8_t)min(nk_, 255u);
           tot += nk_;
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
       }
     }
     if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
-    if (mx > (unsigned)A.L.cap) {
+    if (live && mx > (unsigned)A.L.cap) {
       atomicMax(A.flags, mx);
       if (q < 0) {                          // hand the column to the overflow pass
         const unsigned slot = atomicAdd(A.flags + 1, 1u);

@@ -64,25 +64,30 @@ __device__ __forceinline__ void acc_insert(Acc& A, int& p, float a, float b, int
   ++A.n;
 }
 
-constexpr int P2_R = 8;   // list elements loaded into registers per batch
+constexpr int P2_R = 8;   // list elements loaded per batch
 
 // insert a sorted list (element e at B[e * stride]) into the accumulator, P2_R elements at a
-// time: the batch's loads are independent and issue together
-// (level sets are stored unclipped: each element is clipped to [zlo, zhi] here; clipping
-// commutes with the union)
+// time: the batch's loads are independent and issue together (unrolled), the batch is parked in
+// a per-thread shared scratch and inserted by a rolled loop -- one inlined copy of acc_insert
+// keeps the kernel small enough for the instruction cache.  (Level sets are stored unclipped:
+// each element is clipped to [zlo, zhi] here; clipping commutes with the union.)
 template <int T>
 __device__ __forceinline__ void acc_insert_list(Acc& A, const float2* __restrict__ B, int nb, int64_t stride,
-                                                float zlo, float zhi, int cap, unsigned* need) {
+                                                float2* scratch, float zlo, float zhi, int cap, unsigned* need) {
   int p = 0;
   for (int e0 = 0; e0 < nb; e0 += P2_R) {
+    const int nbat = min(P2_R, nb - e0);
     float2 x[P2_R];
 #pragma unroll
     for (int u = 0; u < P2_R; ++u)
-      if (e0 + u < nb) x[u] = B[(int64_t)(e0 + u) * stride];
+      if (u < nbat) x[u] = B[(int64_t)(e0 + u) * stride];
 #pragma unroll
-    for (int u = 0; u < P2_R; ++u) {
-      if (e0 + u >= nb) continue;
-      const float lo = fmaxf(x[u].x, zlo), hi = fminf(x[u].y, zhi);
+    for (int u = 0; u < P2_R; ++u)
+      if (u < nbat) scratch[u * T] = x[u];
+#pragma unroll 1
+    for (int u = 0; u < nbat; ++u) {
+      const float2 v = scratch[u * T];
+      const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
       if (lo < hi) acc_insert<T>(A, p, lo, hi, cap, need);
     }
   }
@@ -92,8 +97,8 @@ __device__ __forceinline__ void acc_insert_list(Acc& A, const float2* __restrict
 // offset dy = 0, 1, -1, 2, -2, ... the lists U_f(|dy|) (ascending) and U_r(|dy|) (stored
 // descending) of column (i, jg+dy); the two counts of the next row are loaded ahead.
 template <int T>
-__device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A, int cap,
-                                          unsigned* need) {
+__device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A,
+                                          float2* scratch, int cap, unsigned* need) {
   A.n = 0;
   const int dlo = max(-L.R, L.row0 - jg), dhi = min(L.R, L.row0 + L.nrows - 1 - jg);
   const int nt = 2 * L.R + 1;
@@ -110,18 +115,22 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
     c1 = count(t + 1, 1);
     if (n0 + n1 == 0) continue;
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-#pragma unroll
+#pragma unroll 1
     for (int d = 0; d < 2; ++d) {
       const int nb = d ? n1 : n0;
       if (nb == 0) continue;
+      const float2* lb;
+      int64_t st;
       if (nb <= L.cap) {
         const int64_t ts = (int64_t)(L.R + 2) * L.nx;   // one slot
-        acc_insert_list<T>(A, L.z + slot_z_index(L, jl, d, k, d ? nb - 1 : 0, i), nb, d ? -ts : ts, zlo, zhi, cap,
-                           need);
+        lb = L.z + slot_z_index(L, jl, d, k, d ? nb - 1 : 0, i);
+        st = d ? -ts : ts;
       } else {   // the column's lists live in the overflow arena
         const int q = L.ovf_idx[(size_t)jl * L.nx + i];
-        acc_insert_list<T>(A, L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0), nb, d ? -1 : 1, zlo, zhi, cap, need);
+        lb = L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0);
+        st = d ? -1 : 1;
       }
+      acc_insert_list<T>(A, lb, nb, st, scratch, zlo, zhi, cap, need);
     }
   }
 }
@@ -142,7 +151,8 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
   const int i = (int)(cl % nx), jg = row0 + (int)(cl / nx);
   unsigned need = 0;
   Acc U{p2_smem + tid, 0};
-  p2_family<T>(A, i, jg, zlo, zhi, U, acc, &need);
+  float2* scratch = p2_smem + (size_t)acc * T + tid;     // [P2_R][T]
+  p2_family<T>(A, i, jg, zlo, zhi, U, scratch, acc, &need);
   uint32_t n = 0;
   if (OP == OP_DILATE) {
     for (int t = 0; t < U.n; ++t) ostage[(size_t)t * ncol + c] = U.v[t * T];
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
     // at most |U| + |V| - 1 <= 2 acc - 1 intervals and is written behind the reads)
     const int nu = U.n;
     for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * T];
-    p2_family<T>(B, i, jg, zlo, zhi, U, acc, &need);
+    p2_family<T>(B, i, jg, zlo, zhi, U, scratch, acc, &need);
     int p = 0, q = 0;
     float2 u = nu > 0 ? ostage[(size_t)acc * ncol + c] : make_float2(0.f, 0.f);
     while (p < nu && q < U.n) {
@@ -181,7 +191,7 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
 
 inline size_t pass2_smem_bytes(int op, int acc, int T) {
   (void)op;
-  return (size_t)acc * T * sizeof(float2);
+  return (size_t)(acc + P2_R) * T * sizeof(float2);
 }
 inline int pass2_stage_cap(int op, int acc) { return op == OP_SHELL ? 2 * acc : acc + 1; }
 

@@ -326,3 +326,36 @@ print("OK")
     env = dict(os.environ, DEXEL_P1_CAP="2")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+
+
+def test_capsule_pruning_is_exact(dx):
+    """The pass-1 capsule-domination filter (on by default in the ops) drops pieces whose
+    capsule lies inside a neighbour's at every level: results with DEXEL_NO_PRUNE=1 (every
+    piece kept) and without both match the oracle, and the filtered run holds fewer pieces."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
+from oracle.compare import compare
+host = G.config("C2")
+src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
+for op in ("dilate", "erode", "shell"):
+    for r in (4.0, 9.5):
+        if op == "shell":
+            dx.dexel_shell(src, r, r, dst); ref = O.shell(host, r, r)
+        else:
+            getattr(dx, "dexel_" + op)(src, r, dst); ref = getattr(O, op)(host, r)
+        off, ep = dst.download()
+        res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (op, r, res)
+        print(op, r, dst.stats()["n_mid"])
+print("OK")
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    mids = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, DEXEL_NO_PRUNE=flag)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+        mids[flag] = [int(line.split()[-1]) for line in out.stdout.splitlines() if line[:1].isalpha() and line != "OK"]
+    assert all(a < b for a, b in zip(mids["0"], mids["1"])), mids
