@@ -222,8 +222,10 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
   const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) p1_kernel<NWV><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
-  if (NW <= 2) P1(2);
+#define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
+  // small R: the ring-buffered emission variant (measured faster for R < 8, slower above)
+  if (R < 8) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
+  else if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);
   else if (NW <= 9) P1(9);

@@ -156,6 +156,7 @@ __host__ __device__ __forceinline__ size_t piece_index(const PieceSlots& P, int 
 // Pure selection: lo / hi are copies of input values, kappa an integer.
 constexpr int P1_WARPS = 4;
 constexpr int P1_STAGE = 2048;   // keys per warp (8 KB)
+constexpr int P1_RING = 8;       // pending closed pieces per lane
 
 // Capsule domination (prune != nullptr): piece q dominates piece p when kappa_q <= kappa_p and
 //   max(lo_q - lo_p, hi_p - hi_q) <= h(kappa_q, 0) - h(kappa_p, 0),   h(kappa, k) = sqrt(r^2 - (kappa^2+k^2)s^2):
@@ -173,12 +174,14 @@ __device__ __forceinline__ bool dom_margin(float lhs, float rhs) {
   return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs));
 }
 
-template <int NW>
+template <int NW, bool RING>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, int complement, int row0,
                                                             int nrows_out, PieceSlots P, int64_t nlist,
                                                             const float* __restrict__ prune) {
   __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
   __shared__ float h0[256];
+  __shared__ float2 ring_z[P1_WARPS][RING ? P1_RING : 1][32];   // closed pieces awaiting the filter / store
+  __shared__ uint8_t ring_k[P1_WARPS][RING ? P1_RING : 1][32];
   if (prune)
     for (int t = threadIdx.x; t <= R; t += blockDim.x) h0[t] = prune[t];
   __syncthreads();
@@ -269,6 +272,33 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     }
     ++np;
   };
+  // Small R: closed pieces enter a per-lane ring in shared memory (a few predicated
+  // instructions per sweep step); the filter and the global stores run when some lane's ring
+  // is full, once per piece instead of once per step (some lane closes a piece at almost every
+  // step).  Larger R (more work per step elsewhere, fewer closes per step): inline.
+  constexpr bool use_ring = RING;   // host: R < 8
+  const int wid = threadIdx.x >> 5;
+  uint32_t rc = 0, rd = 0;                 // ring: written / drained
+  auto drain = [&]() {
+    const uint32_t nd = __reduce_max_sync(FULL, rc - rd);
+    for (uint32_t u = 0; u < nd; ++u) {
+      if (rd == rc) continue;
+      const float2 v = ring_z[wid][rd % P1_RING][lane];
+      const int kv = ring_k[wid][rd % P1_RING][lane];
+      ++rd;
+      if (!prune) {
+        put(v.x, v.y, kv);
+      } else if (pk == KNONE) {
+        plo = v.x; phi = v.y; pk = kv;
+      } else {
+        const float D = h0[pk] - h0[kv];                    // H[kp] - H[kn]
+        if (pk <= kv && dom_margin(v.y - phi, D)) continue; // the pending piece covers the new one
+        if (!(kv <= pk && dom_margin(v.x - plo, -D))) put(plo, phi, pk);
+        plo = v.x; phi = v.y; pk = kv;
+      }
+    }
+    __syncwarp();
+  };
   for (;;) {
     uint32_t my = KEY_NONE;
 #pragma unroll
@@ -286,7 +316,19 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       }
     }
     const int knew = nearest_parent<NW>(M, lane + R, R);
-    if (knew != kap) {
+    if constexpr (use_ring) {
+      const bool chg = knew != kap;
+      const bool closed = chg && kap != KNONE;
+      const float z = keyf(zk);
+      if (closed) {
+        ring_z[wid][rc % P1_RING][lane] = make_float2(zstart, z);
+        ring_k[wid][rc % P1_RING][lane] = (uint8_t)kap;
+      }
+      rc += closed ? 1u : 0u;
+      kap = chg ? knew : kap;
+      zstart = chg ? z : zstart;
+      if (__any_sync(FULL, rc - rd == (uint32_t)P1_RING)) drain();
+    } else if (knew != kap) {                // inline filter (measured faster for larger R)
       const float z = keyf(zk);
       if (kap != KNONE) {
         if (!prune) {
@@ -307,6 +349,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       zstart = z;
     }
   }
+  if (use_ring) drain();
   if (prune && pk != KNONE) put(plo, phi, pk);
   if (!list_mode) {
     if (out_ok) {

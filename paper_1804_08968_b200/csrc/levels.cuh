@@ -86,6 +86,13 @@ struct LvArgs {
 
 constexpr int LV_T = 128;
 
+// predicated 8-byte store without a branch (the compiler otherwise wraps each level's rare
+// emission in a BSSY/BRA/BSYNC region that some lane of the warp takes almost every step)
+__device__ __forceinline__ void st_pred_f2(float2* p, float x, float y, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.f32 [%0], {%1, %2};\n\t}"
+               :: "l"(p), "f"(x), "f"(y), "r"((int)pred));
+}
+
 // blockIdx.y = level chunk: this thread runs levels k0 .. k0+LMAX-1 of column c.
 // The h table holds -inf where a piece is out of reach (kappa^2 + k^2 > (r/s)^2): then
 // hi + h = -inf and lo - h = +inf leave the running union unchanged without a validity
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
 #define LV_EMIT(k, pred)                                                      \
   {                                                                           \
     const bool ok_ = (pred) && a[k] < b[k];                                   \
-    if (ok_) Zd[min(o[k], olim)] = make_float2(a[k], b[k]);                   \
+    st_pred_f2(Zd + min(o[k], olim), a[k], b[k], ok_);                        \
     o[k] += ok_ ? ostep : 0u;                                                 \
   }
       // null piece: U_f (-inf, -inf), U_r (+inf, +inf), kappa row R+1 (all -inf)
