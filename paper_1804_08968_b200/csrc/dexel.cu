@@ -356,7 +356,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of
   // <= max_chunk (larger chunks cost more in registers/occupancy than they save)
   static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17};
-  int max_chunk = 12;   // measured on B200: 12 <= 17 < 9 at r = 64, equal at r = 16
+  int max_chunk = 17;   // measured on B200 (branch-free emission): 17 beats 12 at r = 16 and 32
   if (const char* e = std::getenv("DEXEL_LV_CHUNK")) max_chunk = std::max(2, std::min(17, std::atoi(e)));
   const int nchunk = (R + 1 + max_chunk - 1) / max_chunk;
   const int per = (R + 1 + nchunk - 1) / nchunk;
@@ -550,10 +550,12 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
     const int Rf = f == 0 ? Ra : Rb;
     row_bytes += (size_t)nx * 2 * ((Rf + 1) + (Rf + 2) * sizeof(float2) * (size_t)lcap);
   }
-  size_t budget = (size_t)32 << 30;   // level slots of one band (all families)
+  // slots of one band (pieces + level sets, all families): fewer, taller bands recompute fewer
+  // halo rows (2R per band); the budget leaves room for the output staging and the caller
+  size_t budget = (size_t)64 << 30;
   {
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 4);
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 2);
   }
   int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
   if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override
