@@ -12,6 +12,7 @@
 // outgrow them are recomputed into an arena by a second, list-driven launch.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace dexel {
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     const int w = lane + 32 * q;
     if (w < W) col_open(src, i0 - R + w, j, complement, cur[q]);
     else { cur[q].base = 0; cur[q].n = 0; cur[q].v = 0; cur[q].vend = 0; }
-    const uint32_t nv = cur[q].vend - cur[q].v;
+    const uint32_t nv = cur[q].vend - cur[q].v + 1;    // + a KEY_NONE sentinel
     uint32_t incl = nv;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     const uint32_t nv = cur[q].vend - cur[q].v;
     if (staged) {
       for (uint32_t t = 0; t < nv; ++t) stage[sb[q] + t] = fkey(col_value(src, cur[q], cur[q].v + t, complement));
+      stage[sb[q] + nv] = KEY_NONE;             // sentinel: the advance needs no bound check
       pos[q] = sb[q];
       end[q] = sb[q] + nv;
     } else {
@@ -299,6 +301,24 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     }
     __syncwarp();
   };
+  // NW == 2 (R <= 16): the closest parent from two 32-bit windows of the 64-bit mask around this
+  // lane's position p = lane + R: the bits at or below p (top-aligned) and at or above p
+  const int pp = lane + R;
+  const int shr = pp < 32 ? pp : pp - 32;          // right window: bits p .. p+31
+  const int shl = pp >= 31 ? pp - 31 : 31 - pp;    // left window: bits p-31 .. p, bit p on top
+  const bool rlow = pp < 32, lhigh = pp >= 31;      // per-lane constants: selects, not branches
+  auto nearest2 = [&](uint32_t m0, uint32_t m1) -> int {
+    const uint32_t rw = __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr);
+    const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
+    const uint32_t lw = lhigh ? la : lb;
+    const int dr = rw ? __ffs(rw) - 1 : KNONE;
+    const int dl = lw ? __clz(lw) : KNONE;
+    const int d = min(dl, dr);
+    return d <= R ? d : KNONE;
+  };
+  // the sweep, versioned on the (warp-uniform) staging decision so the hot loop carries no
+  // global-memory fallback
+  auto sweep = [&](auto stg) {
   for (;;) {
     uint32_t my = KEY_NONE;
 #pragma unroll
@@ -309,13 +329,17 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     for (int q = 0; q < NW; ++q) {
       const bool hit = nkey[q] == zk;
       M[q] ^= __ballot_sync(FULL, hit);
-      if (hit) {
+      if constexpr (decltype(stg)::value) {         // sentinel-terminated lists in shared memory
+        pos[q] += hit ? 1u : 0u;
+        if (hit) nkey[q] = stage[pos[q]];
+      } else if (hit) {
         ++pos[q];
-        nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(col_value(src, cur[q], pos[q], complement)))
-                                  : KEY_NONE;
+        nkey[q] = pos[q] < end[q] ? fkey(col_value(src, cur[q], pos[q], complement)) : KEY_NONE;
       }
     }
-    const int knew = nearest_parent<NW>(M, lane + R, R);
+    int knew;
+    if constexpr (NW == 2) knew = nearest2(M[0], M[1]);
+    else knew = nearest_parent<NW>(M, lane + R, R);
     if constexpr (use_ring) {
       const bool chg = knew != kap;
       const bool closed = chg && kap != KNONE;
@@ -349,6 +373,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       zstart = z;
     }
   }
+  };
+  if (staged) sweep(std::true_type{});
+  else sweep(std::false_type{});
   if (use_ring) drain();
   if (prune && pk != KNONE) put(plo, phi, pk);
   if (!list_mode) {
