@@ -171,6 +171,13 @@ constexpr int P1_RING = 8;       // pending closed pieces per lane
 // kp <= kn and hi_n - hi_p <= H[kp] - H[kn]  (H = h(., 0), fp32).  Both sides are differences
 // of nearby values (error ~2^-24 of the result), and a piece is only dropped with a relative
 // margin of 1e-6, so rounding can keep a dominated piece but never drop a needed one.
+// predicated store of one piece (8-byte z pair + kappa byte) without a branch
+__device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo, float hi, int k, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v2.f32 [%0], {%2, %3};\n\t"
+               "@q st.global.u8 [%1], %4;\n\t}"
+               :: "l"(zp), "l"(kp), "f"(lo), "f"(hi), "r"(k), "r"((int)pred));
+}
+
 __device__ __forceinline__ bool dom_margin(float lhs, float rhs) {
   return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs));
 }
@@ -352,25 +359,34 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       kap = chg ? knew : kap;
       zstart = chg ? z : zstart;
       if (__any_sync(FULL, rc - rd == (uint32_t)P1_RING)) drain();
-    } else if (knew != kap) {                // inline filter (measured faster for larger R)
+    } else {                                 // inline filter, branch-free (measured faster for larger R)
+      const bool chg = knew != kap;
+      const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
-      if (kap != KNONE) {
-        if (!prune) {
-          put(zstart, z, kap);
-        } else if (pk == KNONE) {
-          plo = zstart; phi = z; pk = kap;
-        } else {
-          const float D = h0[pk] - h0[kap];                    // H[kp] - H[kn]
-          if (pk <= kap && dom_margin(z - phi, D)) {
-            // the pending piece covers the new one
-          } else {
-            if (!(kap <= pk && dom_margin(zstart - plo, -D))) put(plo, phi, pk);
-            plo = zstart; phi = z; pk = kap;
-          }
+      if (prune) {                           // warp-uniform
+        const bool hp = pk != KNONE;
+        const float D = h0[pk & 255] - h0[kap & 255];        // H[kp] - H[kn] (garbage when unused)
+        const bool drop_new = hp && pk <= kap && dom_margin(z - phi, D);
+        const bool drop_pend = kap <= pk && dom_margin(zstart - plo, -D);
+        const bool wr = closed && hp && !drop_new && !drop_pend;
+        if (zb) {
+          const size_t t = (size_t)min(np, tmax) * zstep;
+          st_pred_piece(zb + t, kb + t, plo, phi, pk, wr);
         }
+        np += wr ? 1u : 0u;
+        const bool take = closed && !drop_new;
+        plo = take ? zstart : plo;
+        phi = take ? z : phi;
+        pk = take ? kap : pk;
+      } else {
+        if (zb) {
+          const size_t t = (size_t)min(np, tmax) * zstep;
+          st_pred_piece(zb + t, kb + t, zstart, z, kap, closed);
+        }
+        np += closed ? 1u : 0u;
       }
-      kap = knew;
-      zstart = z;
+      kap = chg ? knew : kap;
+      zstart = chg ? z : zstart;
     }
   }
   };
