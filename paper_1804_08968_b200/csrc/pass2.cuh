@@ -71,25 +71,49 @@ constexpr int P2_R = 8;   // list elements loaded per batch
 // a per-thread shared scratch and inserted by a rolled loop -- one inlined copy of acc_insert
 // keeps the kernel small enough for the instruction cache.  (Level sets are stored unclipped:
 // each element is clipped to [zlo, zhi] here; clipping commutes with the union.)
+// one batch (<= P2_R elements) of a sorted list: element e at B[e * stride]
+struct P2Batch {
+  float2 x[P2_R];
+  int n;
+};
+
 template <int T>
-__device__ __forceinline__ void acc_insert_list(Acc& A, const float2* __restrict__ B, int nb, int64_t stride,
-                                                float2* scratch, float zlo, float zhi, int cap, unsigned* need) {
-  int p = 0;
-  for (int e0 = 0; e0 < nb; e0 += P2_R) {
-    const int nbat = min(P2_R, nb - e0);
-    float2 x[P2_R];
+__device__ __forceinline__ void p2_load(P2Batch& X, const float2* __restrict__ B, int nb, int64_t stride) {
+  X.n = min(P2_R, nb);
 #pragma unroll
-    for (int u = 0; u < P2_R; ++u)
-      if (u < nbat) x[u] = B[(int64_t)(e0 + u) * stride];
+  for (int u = 0; u < P2_R; ++u)
+    if (u < X.n) X.x[u] = B[(int64_t)u * stride];
+}
+
+// insert a loaded batch: parked in a per-thread shared scratch and inserted by a rolled loop --
+// one inlined copy of acc_insert keeps the kernel small enough for the instruction cache.
+// (Level sets are stored unclipped: each element is clipped to [zlo, zhi] here; clipping
+// commutes with the union.)
+template <int T>
+__device__ __forceinline__ void p2_insert(Acc& A, int& p, const P2Batch& X, float2* scratch, float zlo, float zhi,
+                                          int cap, unsigned* need) {
 #pragma unroll
-    for (int u = 0; u < P2_R; ++u)
-      if (u < nbat) scratch[u * T] = x[u];
+  for (int u = 0; u < P2_R; ++u)
+    if (u < X.n) scratch[u * T] = X.x[u];
 #pragma unroll 1
-    for (int u = 0; u < nbat; ++u) {
-      const float2 v = scratch[u * T];
-      const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
-      if (lo < hi) acc_insert<T>(A, p, lo, hi, cap, need);
-    }
+  for (int u = 0; u < X.n; ++u) {
+    const float2 v = scratch[u * T];
+    const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
+    if (lo < hi) acc_insert<T>(A, p, lo, hi, cap, need);
+  }
+}
+
+// insert a sorted list whose first batch X is already loaded (the rare rest batch by batch)
+template <int T>
+__device__ __forceinline__ void acc_insert_list(Acc& A, const P2Batch& X0, const float2* __restrict__ B, int nb,
+                                                int64_t stride, float2* scratch, float zlo, float zhi, int cap,
+                                                unsigned* need) {
+  int p = 0;
+  p2_insert<T>(A, p, X0, scratch, zlo, zhi, cap, need);
+  for (int e0 = P2_R; e0 < nb; e0 += P2_R) {
+    P2Batch X;
+    p2_load<T>(X, B + (int64_t)e0 * stride, nb - e0, stride);
+    p2_insert<T>(A, p, X, scratch, zlo, zhi, cap, need);
   }
 }
 
@@ -115,22 +139,28 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
     c1 = count(t + 1, 1);
     if (n0 + n1 == 0) continue;
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-#pragma unroll 1
+    // both lists' first batches are loaded before either is inserted (twice the loads in flight)
+    const float2* lb[2];
+    int64_t st[2];
+    P2Batch X[2];
+#pragma unroll
     for (int d = 0; d < 2; ++d) {
       const int nb = d ? n1 : n0;
-      if (nb == 0) continue;
-      const float2* lb;
-      int64_t st;
       if (nb <= L.cap) {
         const int64_t ts = (int64_t)(L.R + 2) * L.nx;   // one slot
-        lb = L.z + slot_z_index(L, jl, d, k, d ? nb - 1 : 0, i);
-        st = d ? -ts : ts;
+        lb[d] = L.z + slot_z_index(L, jl, d, k, d && nb ? nb - 1 : 0, i);
+        st[d] = d ? -ts : ts;
       } else {   // the column's lists live in the overflow arena
         const int q = L.ovf_idx[(size_t)jl * L.nx + i];
-        lb = L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0);
-        st = d ? -1 : 1;
+        lb[d] = L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0);
+        st[d] = d ? -1 : 1;
       }
-      acc_insert_list<T>(A, lb, nb, st, scratch, zlo, zhi, cap, need);
+      p2_load<T>(X[d], lb[d], nb, st[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const int nb = d ? n1 : n0;
+      if (nb) acc_insert_list<T>(A, X[d], lb[d], nb, st[d], scratch, zlo, zhi, cap, need);
     }
   }
 }
