@@ -380,7 +380,9 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
       return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
     if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
     CK(cudaMemsetAsync(flags, 0, 64, g->stream));
-    LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, ovf_list, ovf_cap, nullptr, 0};
+    static const bool dbg_on = std::getenv("DEXEL_DEBUG") != nullptr;
+    unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
+    LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_cap, nullptr, 0};
     launch(A, ncol);
     CK(cudaGetLastError());
     unsigned hf[2];
@@ -388,6 +390,14 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     CK(cudaStreamSynchronize(g->stream));
     if (hf[0] > (unsigned)LV_OVF_CAP)
       return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
+    if (dbg) {
+      unsigned long long hd[2];
+      CK(cudaMemcpy(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost));
+      unsigned long long tm = 0;
+      CK(cudaMemcpy(&tm, P.total, sizeof(tm), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[dexel] levels rows %d..%d: %llu pieces, %lld columns (mean %.1f), warps %llu, mean warp max %.1f\n",
+                   lr0, lr0 + lrn, tm, (long long)ncol, (double)tm / ncol, hd[1], (double)hd[0] / std::max(1ull, hd[1]));
+    }
     if (hf[1] <= ovf_cap) {
       if (hf[1] > 0) {   // overflow pass: the listed columns' lists, all of them, into the arena
         if ((s = T.get(sizeof(float2) * (size_t)hf[1] * 2 * (R + 1) * LV_OVF_CAP + 16, (void**)&L->ovf_z))) return s;

@@ -78,6 +78,7 @@ struct LvArgs {
   LevelSlots L;
   unsigned* flags;         // [0] longest list seen, [1] overflow columns
   unsigned long long* nlev;  // total level intervals (statistics)
+  unsigned long long* dbg; // diagnostics or nullptr: [0] sum of per-warp max piece counts, [1] warps
   uint32_t* ovf_list;      // main pass: columns with a list longer than cap
   unsigned ovf_list_cap;
   const uint32_t* list;    // overflow pass: the listed columns, written to the overflow arena
@@ -126,6 +127,10 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
   // processes the "null piece", which leaves both running unions unchanged
   const int m_live = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
   const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)m_live);
+  if (A.dbg && (threadIdx.x & 31) == 0) {                 // diagnostics (DEXEL_DEBUG): sum of warp maxima
+    atomicAdd(A.dbg, (unsigned long long)mmax);
+    atomicAdd(A.dbg + 1, 1ull);
+  }
   {   // all 32 lanes run the loop (warp-uniform trip count and __all_sync); dead lanes see m = 0
     const int64_t c = live ? (A.list ? (int64_t)A.list[g] : g) : 0;
     const int q = A.list ? (int)g : -1;
