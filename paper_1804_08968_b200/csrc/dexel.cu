@@ -564,8 +564,20 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   // halo rows (2R per band); the budget leaves room for the output staging and the caller
   size_t budget = (size_t)64 << 30;
   {
+    // free device memory plus what the stream-ordered pool holds but does not use (freed
+    // temporaries of earlier ops stay reserved: the release threshold is kept at max)
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 2);
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      size_t pooled = 0;
+      cudaMemPool_t pool;
+      if (!g_alloc && cudaDeviceGetDefaultMemPool(&pool, src->d.device) == cudaSuccess) {
+        uint64_t res = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && res > used)
+          pooled = (size_t)(res - used);
+      }
+      budget = std::min(budget, (fr + pooled) / 2);
+    }
   }
   int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
   if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override

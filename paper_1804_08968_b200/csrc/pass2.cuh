@@ -169,7 +169,7 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
 // output column c_local of the band is global output column cbase + c_local; the staging
 // array is [t][ncol_total]
 template <int OP, int T>
-__global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, int nx, int row0, int nrows_out,
+__global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelSlots B, int nx, int row0, int nrows_out,
                                                    int64_t cbase, int64_t ncol, float zlo, float zhi, int acc,
                                                    float2* __restrict__ ostage, uint32_t* __restrict__ ocnt,
                                                    unsigned* flags) {
@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(T) pass2s_kernel(LevelSlots A, LevelSlots B, i
     // at most |U| + |V| - 1 <= 2 acc - 1 intervals and is written behind the reads)
     const int nu = U.n;
     for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * T];
-    p2_family<T>(B, i, jg, zlo, zhi, U, scratch, acc, &need);
+    // D_rin(C) only matters inside D_rout(S): an empty D(S) skips it, and its list elements are
+    // clipped to D(S)'s hull instead of [z_lo, z_hi] (fewer insertions, a shorter accumulator)
+    if (nu > 0) p2_family<T>(B, i, jg, U.v[0].x, U.v[(nu - 1) * T].y, U, scratch, acc, &need);
+    else U.n = 0;
     int p = 0, q = 0;
     float2 u = nu > 0 ? ostage[(size_t)acc * ncol + c] : make_float2(0.f, 0.f);
     while (p < nu && q < U.n) {
