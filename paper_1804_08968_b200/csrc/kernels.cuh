@@ -270,9 +270,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   uint32_t np = 0;
   int kap = KNONE;
   float zstart = 0.f;
-  // pending piece of the capsule-domination filter
-  float plo = 0.f, phi = 0.f;
+  // pending piece of the capsule-domination filter (hpk caches H[pk])
+  float plo = 0.f, phi = 0.f, hpk = 0.f;
   int pk = KNONE;
+  uint32_t woff = 0;                       // next slot (float2 / byte offset from zb / kb)
+  const uint32_t wlim = tmax * zstep;      // the spill cell
   auto put = [&](float lo, float hi, int k) {
     if (zb) {
       const uint32_t t = min(np, tmax);
@@ -363,28 +365,29 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       const bool chg = knew != kap;
       const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
+      bool wr;
+      float wlo, whi;
+      int wk;
       if (prune) {                           // warp-uniform
         const bool hp = pk != KNONE;
-        const float D = h0[pk & 255] - h0[kap & 255];        // H[kp] - H[kn] (garbage when unused)
+        const float D = hpk - h0[kap & 255];                  // H[kp] - H[kn] (garbage when unused)
         const bool drop_new = hp && pk <= kap && dom_margin(z - phi, D);
         const bool drop_pend = kap <= pk && dom_margin(zstart - plo, -D);
-        const bool wr = closed && hp && !drop_new && !drop_pend;
-        if (zb) {
-          const size_t t = (size_t)min(np, tmax) * zstep;
-          st_pred_piece(zb + t, kb + t, plo, phi, pk, wr);
-        }
-        np += wr ? 1u : 0u;
+        wr = closed && hp && !drop_new && !drop_pend;
+        wlo = plo; whi = phi; wk = pk;
         const bool take = closed && !drop_new;
         plo = take ? zstart : plo;
         phi = take ? z : phi;
         pk = take ? kap : pk;
+        hpk = take ? h0[kap & 255] : hpk;
       } else {
-        if (zb) {
-          const size_t t = (size_t)min(np, tmax) * zstep;
-          st_pred_piece(zb + t, kb + t, zstart, z, kap, closed);
-        }
-        np += closed ? 1u : 0u;
+        wr = closed;
+        wlo = zstart; whi = z; wk = kap;
       }
+      // running slot offset (32-bit): advances with each stored piece until the spill cell
+      if (zb) st_pred_piece(zb + woff, kb + woff, wlo, whi, wk, wr);
+      np += wr ? 1u : 0u;
+      woff += (wr && woff < wlim) ? zstep : 0u;
       kap = chg ? knew : kap;
       zstart = chg ? z : zstart;
     }
