@@ -365,7 +365,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     if (v >= per) { lmax = v; break; }
   auto launch = [&](const LvArgs& A, int64_t nwork) {
     if (nwork <= 0) return;
-    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk);
+    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk, 2u);   // z: U_f / U_r
     T.prof.pre(K_LEV);
     switch (lmax) {
 #define LV(V) case V: levels_kernel<V><<<grid, LV_T, 0, g->stream>>>(A); break;
@@ -380,6 +380,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
       return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
     if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
     CK(cudaMemsetAsync(flags, 0, 64, g->stream));
+    CK(cudaMemsetAsync(L->ovf_idx, 0xff, sizeof(int32_t) * ncol, g->stream));   // -1: no arena slot
     static const bool dbg_on = std::getenv("DEXEL_DEBUG") != nullptr;
     unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
     LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_cap, nullptr, 0};

@@ -154,8 +154,10 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     uint32_t o[LMAX];   // next slot of level k0+k, as a float2 offset from slot 0 / level k0 of the block
     const uint32_t nx = (uint32_t)A.L.nx, S = (uint32_t)(R + 2) * nx;      // S = one slot (all levels)
     const uint32_t omax = (uint32_t)(A.L.cap - 1) * S + (uint32_t)(R + 1 - k0) * nx;   // the spill cell
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
+    {
+      // blockIdx.z = direction: U_f (0) and U_r (1) run in separate threads, which halves the
+      // live state per thread (registers -> occupancy); each reads the pieces once
+      const int d = blockIdx.z;
       // main pass: slots of (row, d, level k0); overflow pass: the arena lists of slot q
       float2* Zd = q < 0 ? A.L.z + slot_z_index(A.L, row, d, k0, 0, i)
                          : A.L.ovf_z + ovf_z_index(A.L, q, d, k0, 0);
@@ -234,7 +236,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
     if (live && mx > (unsigned)A.L.cap) {
       atomicMax(A.flags, mx);
-      if (q < 0) {                          // hand the column to the overflow pass
+      // hand the column to the overflow pass -- once, whichever direction's thread gets here first
+      if (q < 0 && atomicCAS(A.L.ovf_idx + c, -1, -2) == -1) {
         const unsigned slot = atomicAdd(A.flags + 1, 1u);
         if (slot < A.ovf_list_cap) {
           A.ovf_list[slot] = (uint32_t)c;
