@@ -12,6 +12,7 @@
 // acc) reruns that stage with a larger capacity; the sizes are kept as hints
 // on the handle for later ops.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -66,6 +67,7 @@ struct dexel_grid_s {
   Buf off, ep;
   uint64_t n = 0;
   dexel_stats stats{};
+  unsigned char* pin = nullptr;   // pinned host scratch for the small device->host readbacks
   // capacity hints carried between ops (grown on overflow)
   int lev_cap = 0, p2_acc = 0, p1_cap = 0;
   // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
@@ -82,7 +84,33 @@ __global__ void rebase_offsets(const uint64_t* __restrict__ src, uint64_t n, uin
   if (t <= n) dst[t] = src[t] - src[0] + add;
 }
 
+// host-side diagnostics (DEXEL_DEBUG): seconds spent in allocation calls and stream syncs
+double g_t_alloc = 0.0, g_t_sync = 0.0;
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+inline cudaError_t timed_sync(cudaStream_t st) {
+  const double t = now_s();
+  const cudaError_t e = cudaStreamSynchronize(st);
+  g_t_sync += now_s() - t;
+  return e;
+}
+
+// small device->host readbacks through the handle's pinned buffer (a pageable destination makes
+// cudaMemcpyAsync a staged, host-synchronous copy); offsets are bytes into the 256-byte buffer
+struct Readback {
+  dexel_grid g;
+  cudaError_t err = cudaSuccess;
+  void add(size_t off, const void* dev, size_t bytes) {
+    if (err == cudaSuccess) err = cudaMemcpyAsync(g->pin + off, dev, bytes, cudaMemcpyDeviceToHost, g->stream);
+  }
+  cudaError_t wait() { return err != cudaSuccess ? err : timed_sync(g->stream); }
+  void get(size_t off, void* dst, size_t bytes) const { std::memcpy(dst, g->pin + off, bytes); }
+};
+
 dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
+  const double t0 = now_s();
+  struct Acc { double t0; ~Acc() { g_t_alloc += now_s() - t0; } } acc_{t0};
   b.bytes = bytes;
   b.p = nullptr;
   if (bytes == 0) bytes = 16;
@@ -196,8 +224,10 @@ dexel_status scan_counts(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n
   LAUNCH(T, K_SCAN, scan_sums_exclusive<<<1, SCAN_THREADS, 0, g->stream>>>(sums, ntiles));
   LAUNCH(T, K_SCAN, scan_tiles_write<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums, off));
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(total, off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
+  Readback rb{g};
+  rb.add(0, off + n, sizeof(uint64_t));
+  CK(rb.wait());
+  rb.get(0, total, sizeof(uint64_t));
   T.release(sums);
   return DEXEL_OK;
 }
@@ -267,9 +297,14 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
     CK(cudaGetLastError());
     unsigned hf[3];
     unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(hf, P->flags, sizeof(hf), cudaMemcpyDeviceToHost, g->stream));
-    CK(cudaMemcpyAsync(&tot, P->total, sizeof(tot), cudaMemcpyDeviceToHost, g->stream));
-    CK(cudaStreamSynchronize(g->stream));
+    {
+      Readback rb{g};
+      rb.add(0, P->flags, sizeof(hf));
+      rb.add(16, P->total, sizeof(tot));
+      CK(rb.wait());
+      rb.get(0, hf, sizeof(hf));
+      rb.get(16, &tot, sizeof(tot));
+    }
     if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
       T.release(P->z);
       T.release(P->k);
@@ -287,8 +322,10 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
       T.prof.post();
       CK(cudaGetLastError());
       // the list launch adds the arena columns' (filtered) counts to the total
-      CK(cudaMemcpyAsync(&tot, P->total, sizeof(tot), cudaMemcpyDeviceToHost, g->stream));
-      CK(cudaStreamSynchronize(g->stream));
+      Readback rb{g};
+      rb.add(0, P->total, sizeof(tot));
+      CK(rb.wait());
+      rb.get(0, &tot, sizeof(tot));
     }
     *n_mid += tot;
     return DEXEL_OK;
@@ -324,7 +361,7 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
   float* d0 = *out + h.size();
   CK(cudaMemcpyAsync(*out, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
   CK(cudaMemcpyAsync(d0, h0.data(), sizeof(float) * n1, cudaMemcpyHostToDevice, g->stream));
-  CK(cudaStreamSynchronize(g->stream));  // the host vectors go out of scope
+  CK(timed_sync(g->stream));  // the host vectors go out of scope
   const char* e = std::getenv("DEXEL_NO_PRUNE");
   *prune = (e && std::atoi(e)) ? nullptr : d0;
   return DEXEL_OK;
@@ -387,8 +424,15 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     launch(A, ncol);
     CK(cudaGetLastError());
     unsigned hf[2];
-    CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, g->stream));
-    CK(cudaStreamSynchronize(g->stream));
+    unsigned long long hn = 0;
+    {
+      Readback rb{g};
+      rb.add(0, flags, sizeof(hf));
+      rb.add(16, nlev, sizeof(hn));
+      CK(rb.wait());
+      rb.get(0, hf, sizeof(hf));
+      rb.get(16, &hn, sizeof(hn));
+    }
     if (hf[0] > (unsigned)LV_OVF_CAP)
       return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
     if (dbg) {
@@ -409,10 +453,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
         launch(B, hf[1]);
         CK(cudaGetLastError());
       }
-      unsigned long long hn = 0;
-      CK(cudaMemcpyAsync(&hn, nlev, sizeof(hn), cudaMemcpyDeviceToHost, g->stream));
-      CK(cudaStreamSynchronize(g->stream));
-      *n_lev += hn;
+      *n_lev += hn;   // (the overflow pass adds nothing to the count)
       break;
     }
     // too many long lists: a larger slot capacity pays
@@ -484,6 +525,8 @@ void set_empty(dexel_grid g) {
 }
 
 dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
+  const double op_t0 = now_s();
+  g_t_alloc = g_t_sync = 0.0;
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
   if (src == dst) return fail(DEXEL_EINVAL, "src and dst must be different handles");
   if (!same_geometry(src->d, dst->d)) return fail(DEXEL_EMISMATCH, "src and dst geometry differ");
@@ -626,8 +669,12 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
       }
     }
     unsigned hf[4];
-    CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    {
+      Readback rb{src};
+      rb.add(0, flags, sizeof(hf));
+      CK(rb.wait());
+      rb.get(0, hf, sizeof(hf));
+    }
     if (hf[2] == 0) break;
     // a pass-2 union outgrew the accumulator: rerun the op with a larger one
     T.release(stage);
@@ -666,6 +713,11 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   }
   dst->stats = stats;
   src->stats = stats;
+  if (std::getenv("DEXEL_DEBUG")) {
+    CK(timed_sync(st));
+    std::fprintf(stderr, "[dexel] op wall %.2f ms: allocation calls %.2f ms, stream syncs %.2f ms\n",
+                 1e3 * (now_s() - op_t0), 1e3 * g_t_alloc, 1e3 * g_t_sync);
+  }
   return DEXEL_OK;
 }
 
@@ -725,8 +777,14 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
     }
     g->own_stream = true;
   }
+  if (cudaMallocHost((void**)&g->pin, 256) != cudaSuccess) {
+    if (g->own_stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return fail(DEXEL_ENOMEM, "cudaMallocHost (256 B readback buffer) failed");
+  }
   dexel_status s = dalloc(g, g->off, sizeof(uint64_t) * (g->ncol + 1));
   if (s) {
+    cudaFreeHost(g->pin);
     delete g;
     return s;
   }
@@ -747,7 +805,7 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
   if (on_dev) {
     CK(cudaMemcpyAsync(&first, offsets, 8, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaMemcpyAsync(&last, offsets + ncol, 8, cudaMemcpyDeviceToHost, g->stream));
-    CK(cudaStreamSynchronize(g->stream));
+    CK(timed_sync(g->stream));
   } else {
     first = offsets[0];
     last = offsets[ncol];
@@ -778,7 +836,7 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
   CK(cudaGetLastError());
   unsigned long long hbad = 0;
   CK(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   if (hbad != ~0ull) {
     dfree(g, off);
     dfree(g, ep);
@@ -840,7 +898,7 @@ dexel_status dexel_download_rows(dexel_grid g, int row_begin, int nrows, uint64_
   uint64_t ab[2] = {0, 0};
   CK(cudaMemcpyAsync(&ab[0], (uint64_t*)g->off.p + c0, 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaMemcpyAsync(&ab[1], (uint64_t*)g->off.p + c0 + nc, 8, cudaMemcpyDeviceToHost, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   const uint64_t n = ab[1] - ab[0];
   *n_out = n;
   if (!offsets) return DEXEL_OK;   // size query
@@ -860,7 +918,7 @@ dexel_status dexel_download_rows(dexel_grid g, int row_begin, int nrows, uint64_
   const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (!on_dev) CK(cudaMemcpyAsync(offsets, tmp, sizeof(uint64_t) * (nc + 1), k, g->stream));
   if (n) CK(cudaMemcpyAsync(endpoints, (const float2*)g->ep.p + ab[0], sizeof(float2) * n, k, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   return DEXEL_OK;
 }
 
@@ -893,7 +951,7 @@ dexel_status dexel_download(dexel_grid g, uint64_t* offsets, float* endpoints, u
   const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   CK(cudaMemcpyAsync(offsets, g->off.p, sizeof(uint64_t) * (g->ncol + 1), k, g->stream));
   if (g->n) CK(cudaMemcpyAsync(endpoints, g->ep.p, sizeof(float) * 2 * g->n, k, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   return DEXEL_OK;
 }
 
@@ -932,13 +990,13 @@ dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offset
     CK(cudaMemcpyAsync(z, oz, sizeof(float2) * m, k, g->stream));
     CK(cudaMemcpyAsync(kappa, ok, m, k, g->stream));
   }
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   return DEXEL_OK;
 }
 
 dexel_status dexel_sync(dexel_grid g) {
   if (!g) return fail(DEXEL_EINVAL, "NULL handle");
-  CK(cudaStreamSynchronize(g->stream));
+  CK(timed_sync(g->stream));
   return DEXEL_OK;
 }
 
@@ -953,6 +1011,7 @@ void dexel_destroy(dexel_grid g) {
   }
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
+  if (g->pin) cudaFreeHost(g->pin);
   delete g;
 }
 
