@@ -99,6 +99,17 @@ dexel_status dexel_erode(dexel_grid src, float r, dexel_grid dst);
  * (the thick shell of PAPER.md:58-61, :847-849).  Same rules. */
 dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst);
 
+/* Morphological compositions (the next item of the survey's scope, SURVEY.md 8(f);
+ * PAPER.md:241 "erosion ... dilation of the complement", :841-842 topological cleaning):
+ *   dexel_open:  dst := D_r(E_r(src))   (removes features thinner than 2r)
+ *   dexel_close: dst := E_r(D_r(src))   (fills gaps and holes narrower than 2r)
+ * computed as two ops through an internal temporary handle on src's stream.  With the
+ * neutral boundary (R6), open(S) <= S <= close(S) and both are idempotent up to
+ * fp32 rounding.  Same argument rules as dexel_dilate; a y-slab handle (nranks > 1) returns
+ * DEXEL_EINVAL (the intermediate needs a halo exchange: compose the ops instead). */
+dexel_status dexel_open(dexel_grid src, float r, dexel_grid dst);
+dexel_status dexel_close(dexel_grid src, float r, dexel_grid dst);
+
 /* Attach halo rows (multi-GPU slabs): side 0 = the nrows global rows directly
  * below y0, side 1 = the nrows rows directly above y1 (row-major CSR of
  * nrows*nx columns, same conventions and validation as dexel_upload).  nrows

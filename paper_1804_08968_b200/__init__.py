@@ -23,7 +23,8 @@ DEXEL_OK, DEXEL_EINVAL, DEXEL_ENOMEM, DEXEL_EMISMATCH, DEXEL_EOVERFLOW, DEXEL_EC
 _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA", 6: "ENCCL"}
 
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
-EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_size",
+EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_open", "dexel_close",
+           "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows"]
@@ -75,6 +76,8 @@ def lib():
             "dexel_dilate": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_erode": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_shell": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_open": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_close": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_size": ([vp, u64p], ctypes.c_int),
             "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
             "dexel_pass1": ([vp, ctypes.c_float, ctypes.c_int, vp, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
@@ -288,4 +291,33 @@ def dexel_pass1(src: Grid, r: float, complement: bool = False):
     return off, z[:2 * m.value], k[:m.value]
 
 
+def dexel_open(src: Grid, r: float, dst: Grid) -> Grid:
+    """dst := D_r(E_r(src)) (opening; PAPER.md:241, :841-842)."""
+    _check(lib().dexel_open(src.h, float(r), dst.h))
+    return dst
+
+
+def dexel_close(src: Grid, r: float, dst: Grid) -> Grid:
+    """dst := E_r(D_r(src)) (closing)."""
+    _check(lib().dexel_close(src.h, float(r), dst.h))
+    return dst
+
+
+def clean(src: Grid, r: float, dst: Grid, order: str = "open-close") -> Grid:
+    """Topological cleaning (fig. cleaning): an opening followed by a
+    closing ("open-close", removes thin features then fills thin gaps) or the reverse."""
+    tmp = Grid.like(src)
+    try:
+        if order == "open-close":
+            dexel_open(src, r, tmp)
+            dexel_close(tmp, r, dst)
+        else:
+            dexel_close(src, r, tmp)
+            dexel_open(tmp, r, dst)
+    finally:
+        tmp.close()
+    return dst
+
+
 dilate, erode, shell, pass1 = dexel_dilate, dexel_erode, dexel_shell, dexel_pass1
+opening, closing = dexel_open, dexel_close

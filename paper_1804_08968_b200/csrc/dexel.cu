@@ -937,6 +937,49 @@ dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst
   return run_op(OP_SHELL, src, r_out, r_in, dst);
 }
 
+}  // extern "C"
+
+namespace {
+// morphological compositions: first op into a
+// temporary handle of the same geometry, second op from it into dst
+dexel_status compose(int op1, int op2, dexel_grid src, float r, dexel_grid dst) {
+  if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
+  if (src == dst) return fail(DEXEL_EINVAL, "src and dst must be different handles");
+  if (src->d.nranks > 1)
+    return fail(DEXEL_EINVAL, "opening/closing of a y-slab needs the intermediate's halo rows: compose "
+                              "dexel_erode/dexel_dilate with a halo exchange in between");
+  dexel_desc d = src->d;
+  d.stream = (void*)src->stream;
+  dexel_grid tmp = nullptr;
+  dexel_status s = dexel_create(&d, &tmp);
+  if (s) return s;
+  tmp->lev_cap = src->lev_cap;
+  tmp->p1_cap = src->p1_cap;
+  tmp->p2_acc = src->p2_acc;
+  s = run_op(op1, src, r, r, tmp);
+  if (!s) {
+    s = run_op(op2, tmp, r, r, dst);
+    src->lev_cap = std::max(src->lev_cap, tmp->lev_cap);
+    src->p1_cap = std::max(src->p1_cap, tmp->p1_cap);
+    src->p2_acc = std::max(src->p2_acc, tmp->p2_acc);
+  }
+  dexel_destroy(tmp);
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+dexel_status dexel_open(dexel_grid src, float r, dexel_grid dst) {
+  g_err.clear();
+  return compose(OP_ERODE, OP_DILATE, src, r, dst);
+}
+
+dexel_status dexel_close(dexel_grid src, float r, dexel_grid dst) {
+  g_err.clear();
+  return compose(OP_DILATE, OP_ERODE, src, r, dst);
+}
+
 dexel_status dexel_size(dexel_grid g, uint64_t* n) {
   if (!g || !n) return fail(DEXEL_EINVAL, "NULL argument");
   *n = g->n;

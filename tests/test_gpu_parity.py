@@ -359,3 +359,71 @@ print("OK")
         assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
         mids[flag] = [int(line.split()[-1]) for line in out.stdout.splitlines() if line[:1].isalpha() and line != "OK"]
     assert all(a < b for a, b in zip(mids["0"], mids["1"])), mids
+
+
+# ---------------------------------------------------------------- openings / closings (NEXT #1)
+def _to_host_grid(host, res):
+    """an oracle Result as an fp32 canonical input grid (touching after rounding: merged)."""
+    off = np.asarray(res.off, dtype=np.int64)
+    z = np.asarray(res.z, dtype=np.float64).reshape(-1, 2)
+    cols = []
+    for c in range(host.ncol):
+        iv = z[off[c]:off[c + 1]].astype(np.float32)
+        out = []
+        for a, b in iv:
+            if not a < b:
+                continue
+            if out and a <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], b)
+            else:
+                out.append([a, b])
+        cols.append(np.array(out, dtype=np.float32).reshape(-1, 2))
+    return G.from_columns(host.nx, host.ny, cols, host.z_lo, host.z_hi, getattr(host, "z_ref", 0.0))
+
+
+def _contained(off_a, ep_a, off_b, ep_b, tau=TAU):
+    """every interval of A lies inside some interval of B (up to tau), column by column."""
+    za, zb = np.asarray(ep_a, np.float64).reshape(-1, 2), np.asarray(ep_b, np.float64).reshape(-1, 2)
+    for c in range(len(off_a) - 1):
+        A = za[int(off_a[c]):int(off_a[c + 1])]
+        B = zb[int(off_b[c]):int(off_b[c + 1])]
+        for a, b in A:
+            if b - a < tau:
+                continue
+            if not any(lo - tau <= a and b <= hi + tau for lo, hi in B):
+                return False
+    return True
+
+
+@pytest.mark.parametrize("name_or_seed,r", [("C1", 3.0), (11, 2.0), (12, 3.5), (13, 1.0)])
+def test_open_close_match_oracle_composition(dx, name_or_seed, r):
+    """dexel_open = D_r(E_r(S)) and dexel_close = E_r(D_r(S)) (PAPER.md:241, :841-842) match
+    the oracle's composition; open(S) <= S <= close(S); both idempotent (within tau)."""
+    if isinstance(name_or_seed, str):
+        host = G.config(name_or_seed)
+    else:
+        host = G.random_grid(23, 19, 4, -9.0, 9.0, name_or_seed)
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    dst2 = dx.Grid.like(src)
+    for op, first, second in (("open", O.erode, O.dilate), ("close", O.dilate, O.erode)):
+        getattr(dx, "dexel_" + op)(src, r, dst)
+        off, ep = dst.download()
+        ref = second(_to_host_grid(host, first(host, r)), r)
+        check(off, ep, ref, what=f"{op} r={r}")
+        # idempotence
+        getattr(dx, "dexel_" + op)(dst, r, dst2)
+        off2, ep2 = dst2.download()
+        res = compare(off2, ep2, off, ep, TAU)
+        assert res["ok"], (op, "not idempotent", res)
+        if op == "open":
+            assert _contained(off, ep, host.off, host.ep), "opening not inside S"
+        else:
+            assert _contained(host.off, host.ep, off, ep), "S not inside its closing"
+    # topological cleaning composes the two
+    dx.clean(src, r, dst2)
+    off, ep = dst2.download()
+    ref = O.erode(_to_host_grid(host, O.dilate(_to_host_grid(host, O.dilate(_to_host_grid(host, O.erode(host, r)), r)), r)), r)
+    check(off, ep, ref, what=f"clean r={r}")
+    for g in (src, dst, dst2):
+        g.close()
