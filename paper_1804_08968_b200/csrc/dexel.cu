@@ -402,7 +402,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     if (v >= per) { lmax = v; break; }
   auto launch = [&](const LvArgs& A, int64_t nwork) {
     if (nwork <= 0) return;
-    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk, 2u);   // z: U_f / U_r
+    const dim3 grid((unsigned)((nwork + 63) / 64), (unsigned)nchunk);   // 64 columns x 2 directions per block
     T.prof.pre(K_LEV);
     switch (lmax) {
 #define LV(V) case V: levels_kernel<V><<<grid, LV_T, 0, g->stream>>>(A); break;

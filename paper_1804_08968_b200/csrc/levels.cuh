@@ -118,9 +118,17 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     const float h = (kap <= R && kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
     Hs[t] = h >= 0.f ? h : -INFINITY;
   }
+  __shared__ uint16_t cntS[2][LMAX][64];          // both directions' list lengths of the block's columns
+  __shared__ uint8_t ovfS[2][64];                  // a direction outgrew its slots (no merge)
   __syncthreads();
   uint32_t tot = 0, mx = 0;
-  const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
+  int tot_adj = 0;
+  // block = 64 columns x 2 directions: warps 0-1 run U_f (d = 0), warps 2-3 U_r (d = 1) of the
+  // same 64 columns (halves the live state per thread); afterwards they merge U_f(k) and U_r(k)
+  // into L_k in place
+  const int d = threadIdx.x >> 6;
+  const int lc = threadIdx.x & 63;
+  const int64_t g = (int64_t)blockIdx.x * 64 + lc;
   const bool live = g < (A.list ? A.nlist : A.ncol);
   // every lane of the warp walks the same piece index t (0..mmax-1 forward, mmax-1..0 backward):
   // the slot reads stay coalesced and the loop never diverges; a lane past its own count
@@ -155,9 +163,6 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     const uint32_t nx = (uint32_t)A.L.nx, S = (uint32_t)(R + 2) * nx;      // S = one slot (all levels)
     const uint32_t omax = (uint32_t)(A.L.cap - 1) * S + (uint32_t)(R + 1 - k0) * nx;   // the spill cell
     {
-      // blockIdx.z = direction: U_f (0) and U_r (1) run in separate threads, which halves the
-      // live state per thread (registers -> occupancy); each reads the pieces once
-      const int d = blockIdx.z;
       // main pass: slots of (row, d, level k0); overflow pass: the arena lists of slot q
       float2* Zd = q < 0 ? A.L.z + slot_z_index(A.L, row, d, k0, 0, i)
                          : A.L.ovf_z + ovf_z_index(A.L, q, d, k0, 0);
@@ -225,14 +230,60 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
       for (int k = 0; k < LMAX; ++k) {
         LV_EMIT(k, true);
 #undef LV_EMIT
+        const uint32_t nk_ = (o[k] - (uint32_t)k * olev) / ostep;
+        cntS[d][k][lc] = (uint16_t)min(nk_, 65535u);
         if (live && k0 + k <= R) {
-          const uint32_t nk_ = (o[k] - (uint32_t)k * olev) / ostep;
           if (q < 0) A.L.cnt[slot_cnt_index(A.L, row, d, k0 + k, i)] = (uint8_t)min(nk_, 255u);
           tot += nk_;
           mx = max(mx, nk_);
         }
       }
     }
+    ovfS[d][lc] = (uint8_t)(mx > (unsigned)A.L.cap);
+    __syncthreads();
+    // L_k = U_f(k) u U_r(k), merged in place into U_f's slots: every component
+    // of L_k contains a U_f component, so |L_k| <= |U_f(k)| and the write index never passes the
+    // read index.  U_r's count becomes 0 -- pass 2 then reads one list per (row, level) instead of
+    // two.  Each direction's threads merge half of the levels; columns whose lists went to the
+    // overflow arena keep both lists (pass 2 reads both).
+    if (live && q < 0 && !ovfS[0][lc] && !ovfS[1][lc]) {
+      const int64_t ts = (int64_t)(R + 2) * A.L.nx;     // one slot
+      for (int k = d; k < LMAX; k += 2) {
+        if (k0 + k > R) break;
+        const int nf = cntS[0][k][lc], nr = cntS[1][k][lc];
+        if (nr == 0) continue;
+        float2* F = A.L.z + slot_z_index(A.L, row, 0, k0 + k, 0, i);
+        const float2* Rl = A.L.z + slot_z_index(A.L, row, 1, k0 + k, 0, i);   // stored descending
+        int fi = 0, ri = nr - 1, w = 0;
+        float2 xf = nf > 0 ? F[0] : make_float2(INFINITY, INFINITY);
+        float2 xr = Rl[(int64_t)ri * ts];
+        float cs = 0.f, ce = 0.f;
+        bool have = false;
+        while (fi < nf || ri >= 0) {
+          float2 x;
+          if (ri < 0 || (fi < nf && xf.x <= xr.x)) {
+            x = xf;
+            if (++fi < nf) xf = F[(int64_t)fi * ts];
+          } else {
+            x = xr;
+            if (--ri >= 0) xr = Rl[(int64_t)ri * ts];
+          }
+          if (!have) {
+            cs = x.x; ce = x.y; have = true;
+          } else if (x.x <= ce) {
+            ce = fmaxf(ce, x.y);
+          } else {
+            F[(int64_t)(w++) * ts] = make_float2(cs, ce);
+            cs = x.x; ce = x.y;
+          }
+        }
+        if (have) F[(int64_t)(w++) * ts] = make_float2(cs, ce);
+        A.L.cnt[slot_cnt_index(A.L, row, 0, k0 + k, i)] = (uint8_t)w;
+        A.L.cnt[slot_cnt_index(A.L, row, 1, k0 + k, i)] = 0;
+        tot_adj += w - nf - nr;
+      }
+    }
+    tot += (uint32_t)tot_adj;              // (level intervals as stored, after the merge)
     if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
     if (live && mx > (unsigned)A.L.cap) {
       atomicMax(A.flags, mx);
