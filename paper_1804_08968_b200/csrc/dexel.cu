@@ -3,13 +3,12 @@
 //
 // Op pipeline (one "family" per dilation; erode and shell dilate the
 // complement, which pass 1 reads on the fly):
-//   pass1 COUNT -> scan -> pass1 WRITE     S_In -> S_Mid (pieces lo,hi,kappa), CSR
-//   levels (envelope)                      S_Mid -> level slots L_k, k = 0..R
+//   pass1 (slots; rare list pass)          S_In -> S_Mid (pieces lo,hi,kappa)
+//   levels (forward stack sweep)           S_Mid -> level slots L_k, k = 0..R
 //   pass2 (+ epilogue) -> scan -> compact  {L_k} -> S_Out (output CSR)
 // Host synchronisations per family: the pass-1 total (allocation size) and the
 // level kernel's capacity flags; per op: the pass-2 flags and the output total.
-// A capacity overflow (level list > cap, envelope deque > D, pass-2 union >
-// acc) reruns that stage with a larger capacity; the sizes are kept as hints
+// A capacity overflow (piece slots, level list > cap, pass-2 union > acc) reruns that stage with a larger capacity; the sizes are kept as hints
 // on the handle for later ops.
 #include <algorithm>
 #include <chrono>
@@ -384,8 +383,8 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   L->nrows = lrn;
   L->row0 = lr0;
   L->cap = g->lev_cap > 0 ? g->lev_cap : 8;
-  const size_t nlist = (size_t)ncol * 2 * (R + 1);
-  if ((s = T.get(nlist + 16, (void**)&L->cnt))) return s;
+  const size_t nlist = (size_t)ncol * (R + 1);
+  if ((s = T.get(sizeof(uint16_t) * nlist + 16, (void**)&L->cnt))) return s;
   if ((s = T.get(sizeof(int32_t) * ncol + 16, (void**)&L->ovf_idx))) return s;
   const unsigned ovf_cap = (unsigned)std::max<int64_t>(256, ncol / 256);
   uint32_t* ovf_list = nullptr;
@@ -402,7 +401,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     if (v >= per) { lmax = v; break; }
   auto launch = [&](const LvArgs& A, int64_t nwork) {
     if (nwork <= 0) return;
-    const dim3 grid((unsigned)((nwork + 63) / 64), (unsigned)nchunk);   // 64 columns x 2 directions per block
+    const dim3 grid((unsigned)((nwork + LV_T - 1) / LV_T), (unsigned)nchunk);
     T.prof.pre(K_LEV);
     switch (lmax) {
 #define LV(V) case V: levels_kernel<V><<<grid, LV_T, 0, g->stream>>>(A); break;
@@ -412,8 +411,8 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     T.prof.post();
   };
   for (int attempt = 0; attempt < 6; ++attempt) {
-    const size_t nslot = (size_t)ncol * 2 * (R + 2) * L->cap;   // + the spill level per (row, d)
-    if ((size_t)(R + 2) * L->cap * src.nx >= (1ull << 32))
+    const size_t nslot = (size_t)ncol * (R + 2) * (L->cap + 1);   // + the dummy slot, the spill level
+    if ((size_t)(R + 2) * (L->cap + 1) * src.nx >= (1ull << 32))
       return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
     if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
     CK(cudaMemsetAsync(flags, 0, 64, g->stream));
@@ -445,13 +444,23 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     }
     if (hf[1] <= ovf_cap) {
       if (hf[1] > 0) {   // overflow pass: the listed columns' lists, all of them, into the arena
-        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * 2 * (R + 1) * LV_OVF_CAP + 16, (void**)&L->ovf_z))) return s;
+        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * (R + 1) * (LV_OVF_CAP + 1) + 16, (void**)&L->ovf_z)))
+          return s;
         LvArgs B = A;
         B.L = *L;
         B.list = ovf_list;
         B.nlist = hf[1];
         launch(B, hf[1]);
         CK(cudaGetLastError());
+        // a list that outgrows the arena (255) only shows there when the sweep popped back
+        // below the capacity in the main pass
+        Readback rb{g};
+        rb.add(0, flags, sizeof(unsigned));
+        CK(rb.wait());
+        unsigned f0 = 0;
+        rb.get(0, &f0, sizeof(f0));
+        if (f0 > (unsigned)LV_OVF_CAP)
+          return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
       }
       *n_lev += hn;   // (the overflow pass adds nothing to the count)
       break;
@@ -602,7 +611,7 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   size_t row_bytes = (size_t)nx * ((size_t)(pcap + 1) * (sizeof(float2) + 1) + 8);
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
-    row_bytes += (size_t)nx * 2 * ((Rf + 1) + (Rf + 2) * sizeof(float2) * (size_t)lcap);
+    row_bytes += (size_t)nx * ((Rf + 1) * sizeof(uint16_t) + (Rf + 2) * sizeof(float2) * (size_t)(lcap + 1));
   }
   // slots of one band (pieces + level sets, all families): fewer, taller bands recompute fewer
   // halo rows (2R per band); the budget leaves room for the output staging and the caller

@@ -118,8 +118,9 @@ __device__ __forceinline__ void acc_insert_list(Acc& A, const P2Batch& X0, const
 }
 
 // union over dy of one family's level lists for output column (i, jg): for each row
-// offset dy = 0, 1, -1, 2, -2, ... the lists U_f(|dy|) (ascending) and U_r(|dy|) (stored
-// descending) of column (i, jg+dy); the two counts of the next row are loaded ahead.
+// offset dy = 0, 1, -1, 2, -2, ... the list L_|dy| of column (i, jg+dy).  The next row's
+// first batch is loaded before the current row is inserted (two rows' loads in flight), and
+// counts are read one row further ahead.
 template <int T>
 __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A,
                                           float2* scratch, int cap, unsigned* need) {
@@ -127,41 +128,41 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
   const int dlo = max(-L.R, L.row0 - jg), dhi = min(L.R, L.row0 + L.nrows - 1 - jg);
   const int nt = 2 * L.R + 1;
   auto dy_of = [](int t) { return (t & 1) ? ((t + 1) >> 1) : -(t >> 1); };
-  auto count = [&](int t, int d) -> int {
+  auto count = [&](int t) -> int {
     if (t >= nt) return 0;
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy;
-    return (dy < dlo || dy > dhi) ? 0 : L.cnt[slot_cnt_index(L, jg + dy - L.row0, d, k, i)];
+    return (dy < dlo || dy > dhi) ? 0 : (int)L.cnt[slot_cnt_index(L, jg + dy - L.row0, k, i)];
   };
-  int c0 = count(0, 0), c1 = count(0, 1);
-  for (int t = 0; t < nt; ++t) {
-    const int n0 = c0, n1 = c1;
-    c0 = count(t + 1, 0);
-    c1 = count(t + 1, 1);
-    if (n0 + n1 == 0) continue;
+  // list of row offset t (count word cw != 0): first element's address and stride, first batch
+  // loaded; returns the list length
+  auto open = [&](int t, int cw, const float2*& lb, int64_t& st, P2Batch& X) -> int {
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-    // both lists' first batches are loaded before either is inserted (twice the loads in flight)
-    const float2* lb[2];
-    int64_t st[2];
-    P2Batch X[2];
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const int nb = d ? n1 : n0;
-      if (nb <= L.cap) {
-        const int64_t ts = (int64_t)(L.R + 2) * L.nx;   // one slot
-        lb[d] = L.z + slot_z_index(L, jl, d, k, d && nb ? nb - 1 : 0, i);
-        st[d] = d ? -ts : ts;
-      } else {   // the column's lists live in the overflow arena
-        const int q = L.ovf_idx[(size_t)jl * L.nx + i];
-        lb[d] = L.ovf_z + ovf_z_index(L, q, d, k, d ? nb - 1 : 0);
-        st[d] = d ? -1 : 1;
-      }
-      p2_load<T>(X[d], lb[d], nb, st[d]);
+    const int nb = cw & 0xff;
+    if (!(cw & LV_IN_ARENA)) {
+      lb = L.z + slot_z_index(L, jl, k, 1, i);
+      st = (int64_t)(L.R + 2) * L.nx;   // one slot
+    } else {   // the column's lists live in the overflow arena
+      lb = L.ovf_z + ovf_z_index(L, L.ovf_idx[(size_t)jl * L.nx + i], k, 1);
+      st = 1;
     }
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const int nb = d ? n1 : n0;
-      if (nb) acc_insert_list<T>(A, X[d], lb[d], nb, st[d], scratch, zlo, zhi, cap, need);
-    }
+    p2_load<T>(X, lb, nb, st);
+    return nb;
+  };
+  int cw = count(0), cwn = count(1), n = 0;
+  const float2* lb = nullptr;
+  int64_t st = 0;
+  P2Batch X;
+  X.n = 0;
+  if (cw & 0xff) n = open(0, cw, lb, st, X);
+  for (int t = 0; t < nt; ++t) {
+    const int nc = n;
+    const float2* lbc = lb;
+    const int64_t stc = st;
+    const P2Batch Xc = X;
+    cw = cwn;
+    cwn = count(t + 2);
+    n = (cw & 0xff) ? open(t + 1, cw, lb, st, X) : 0;
+    if (nc) acc_insert_list<T>(A, Xc, lbc, nc, stc, scratch, zlo, zhi, cap, need);
   }
 }
 
