@@ -253,7 +253,11 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
   if (blocks == 0) return;
 #define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
   // small R: the ring-buffered emission variant (measured faster for R < 8, slower above)
-  if (R < 8) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
+  static const int ring_below = [] {
+    const char* e = std::getenv("DEXEL_P1_RING_BELOW");   // experiment override
+    return e ? std::atoi(e) : 8;
+  }();
+  if (R < ring_below && NW <= 2) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
   else if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);

@@ -188,10 +188,28 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
                                                             const float* __restrict__ prune) {
   __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
   __shared__ float h0[256];
+  // NW == 2 (R <= 16), inline filter: both domination thresholds of every (pending kappa,
+  // new kappa) pair, margin included: x for "new dominates pending", y for "pending
+  // dominates new"; -inf where the kappa order rules the test out, in the row of "no pending
+  // piece" (17) and the column of KNONE (31)
+  __shared__ float2 thr[(NW == 2 && !RING) ? 18 * 32 : 1];
   __shared__ float2 ring_z[P1_WARPS][RING ? P1_RING : 1][32];   // closed pieces awaiting the filter / store
   __shared__ uint8_t ring_k[P1_WARPS][RING ? P1_RING : 1][32];
-  if (prune)
+  if (prune) {
     for (int t = threadIdx.x; t <= R; t += blockDim.x) h0[t] = prune[t];
+    if constexpr (NW == 2 && !RING) {
+      for (int t = threadIdx.x; t < 18 * 32; t += blockDim.x) {
+        const int kp = t >> 5, kn = t & 31;
+        float2 v = make_float2(-INFINITY, -INFINITY);
+        if (kp <= R && kn <= R) {
+          const float D = prune[kp] - prune[kn];                // H[kp] - H[kn]
+          if (kp <= kn) v.x = D - 1e-6f * (1.0f + fabsf(D));    // drop new:     hi_n - hi_p <= x
+          if (kn <= kp) v.y = -D - 1e-6f * (1.0f + fabsf(D));   // drop pending: lo_n - lo_p <= y
+        }
+        thr[t] = v;
+      }
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   uint32_t* stage = stage_all[threadIdx.x >> 5];
@@ -247,21 +265,24 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   const bool out_ok = i < src.nx;
   const int64_t c = (int64_t)jr * src.nx + i;
   // where this lane's pieces go: slots (main pass), the arena (list mode, overflow columns), nowhere
-  float2* zb = nullptr;
-  uint8_t* kb = nullptr;
+  float2* zb = P.z;                      // (a valid address even where nothing is stored)
+  uint8_t* kb = P.k;
   uint32_t zstep = 0, tmax = 0;
+  bool has_out = false;
   if (out_ok) {
     if (!list_mode) {
       zb = P.z + piece_index(P, jr, 0, i);
       kb = P.k + piece_index(P, jr, 0, i);
       zstep = (uint32_t)P.nx;
       tmax = (uint32_t)P.cap;                      // spill cell
+      has_out = true;
     } else if (P.ovf_idx[c] >= 0) {
       const size_t q = (size_t)P.ovf_idx[c] * P.ovf_cap;
       zb = P.ovf_z + q;
       kb = P.ovf_k + q;
       zstep = 1;
       tmax = (uint32_t)P.ovf_cap - 1;
+      has_out = true;
     }
   }
   uint32_t M[NW];
@@ -276,7 +297,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   uint32_t woff = 0;                       // next slot (float2 / byte offset from zb / kb)
   const uint32_t wlim = tmax * zstep;      // the spill cell
   auto put = [&](float lo, float hi, int k) {
-    if (zb) {
+    if (has_out) {
       const uint32_t t = min(np, tmax);
       zb[(size_t)t * zstep] = make_float2(lo, hi);
       kb[(size_t)t * zstep] = (uint8_t)k;
@@ -365,29 +386,33 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       const bool chg = knew != kap;
       const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
-      bool wr;
-      float wlo, whi;
-      int wk;
       if (prune) {                           // warp-uniform
         const bool hp = pk != KNONE;
-        const float D = hpk - h0[kap & 255];                  // H[kp] - H[kn] (garbage when unused)
-        const bool drop_new = hp && pk <= kap && dom_margin(z - phi, D);
-        const bool drop_pend = kap <= pk && dom_margin(zstart - plo, -D);
-        wr = closed && hp && !drop_new && !drop_pend;
-        wlo = plo; whi = phi; wk = pk;
+        bool drop_new, drop_pend;
+        if constexpr (NW == 2) {             // thresholds from the (kp, kn) table
+          const float2 th = thr[min(pk, 17) * 32 + (kap & 31)];
+          drop_new = z - phi <= th.x;
+          drop_pend = zstart - plo <= th.y;
+        } else {
+          const float D = hpk - h0[kap & 255];                  // H[kp] - H[kn] (garbage when unused)
+          drop_new = hp && pk <= kap && dom_margin(z - phi, D);
+          drop_pend = kap <= pk && dom_margin(zstart - plo, -D);
+          hpk = (closed && !drop_new) ? h0[kap & 255] : hpk;
+        }
+        // the pending piece is stored (unless the new one dominates it) before it is replaced
+        const bool wr = closed && hp && !drop_new && !drop_pend;
+        st_pred_piece(zb + woff, kb + woff, plo, phi, pk, wr && has_out);
+        np += wr ? 1u : 0u;
+        woff += (wr && woff < wlim) ? zstep : 0u;
         const bool take = closed && !drop_new;
         plo = take ? zstart : plo;
         phi = take ? z : phi;
         pk = take ? kap : pk;
-        hpk = take ? h0[kap & 255] : hpk;
       } else {
-        wr = closed;
-        wlo = zstart; whi = z; wk = kap;
+        st_pred_piece(zb + woff, kb + woff, zstart, z, kap, closed && has_out);
+        np += closed ? 1u : 0u;
+        woff += (closed && woff < wlim) ? zstep : 0u;
       }
-      // running slot offset (32-bit): advances with each stored piece until the spill cell
-      if (zb) st_pred_piece(zb + woff, kb + woff, wlo, whi, wk, wr);
-      np += wr ? 1u : 0u;
-      woff += (wr && woff < wlim) ? zstep : 0u;
       kap = chg ? knew : kap;
       zstart = chg ? z : zstart;
     }
@@ -415,7 +440,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     }
     const unsigned wsum = __reduce_add_sync(FULL, (out_ok && np <= (uint32_t)P.cap) ? np : 0u);   // arena: list launch
     if (lane == 0 && wsum) atomicAdd(P.total, (unsigned long long)wsum);
-  } else if (zb) {
+  } else if (has_out) {
     P.cnt[c] = np;                                   // the filtered count of an arena column
     atomicAdd(P.total, (unsigned long long)np);
   }
