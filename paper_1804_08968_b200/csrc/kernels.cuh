@@ -264,9 +264,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   const int i = i0 + lane;
   const bool out_ok = i < src.nx;
   const int64_t c = (int64_t)jr * src.nx + i;
-  // where this lane's pieces go: slots (main pass), the arena (list mode, overflow columns), nowhere
-  float2* zb = P.z;                      // (a valid address even where nothing is stored)
-  uint8_t* kb = P.k;
+  // where this lane's pieces go: slots (main pass), the arena (list mode, overflow columns), or
+  // nowhere -- then the stores go to a spill cell (slot cap of a column of this row, never read),
+  // so the store predicate needs no extra term
+  float2* zb = P.z + piece_index(P, jr, P.cap, out_ok ? i : 0);
+  uint8_t* kb = P.k + piece_index(P, jr, P.cap, out_ok ? i : 0);
   uint32_t zstep = 0, tmax = 0;
   bool has_out = false;
   if (out_ok) {
@@ -337,18 +339,17 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   const int shr = pp < 32 ? pp : pp - 32;          // right window: bits p .. p+31
   const int shl = pp >= 31 ? pp - 31 : 31 - pp;    // left window: bits p-31 .. p, bit p on top
   const bool rlow = pp < 32, lhigh = pp >= 31;      // per-lane constants: selects, not branches
+  // (a sentinel bit at distance 31 > R keeps both windows non-zero: no zero tests)
   auto nearest2 = [&](uint32_t m0, uint32_t m1) -> int {
-    const uint32_t rw = __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr);
+    const uint32_t rw = __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr) | 0x80000000u;
     const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
-    const uint32_t lw = lhigh ? la : lb;
-    const int dr = rw ? __ffs(rw) - 1 : KNONE;
-    const int dl = lw ? __clz(lw) : KNONE;
-    const int d = min(dl, dr);
+    const uint32_t lw = (lhigh ? la : lb) | 1u;
+    const int d = min(__clz(lw), __ffs(rw) - 1);
     return d <= R ? d : KNONE;
   };
   // the sweep, versioned on the (warp-uniform) staging decision so the hot loop carries no
   // global-memory fallback
-  auto sweep = [&](auto stg) {
+  auto sweep = [&](auto stg, auto prn) {
   for (;;) {
     uint32_t my = KEY_NONE;
 #pragma unroll
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       const bool chg = knew != kap;
       const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
-      if (prune) {                           // warp-uniform
+      if constexpr (decltype(prn)::value) {   // (the sweep is versioned on prune != nullptr)
         const bool hp = pk != KNONE;
         bool drop_new, drop_pend;
         if constexpr (NW == 2) {             // thresholds from the (kp, kn) table
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
         }
         // the pending piece is stored (unless the new one dominates it) before it is replaced
         const bool wr = closed && hp && !drop_new && !drop_pend;
-        st_pred_piece(zb + woff, kb + woff, plo, phi, pk, wr && has_out);
+        st_pred_piece(zb + woff, kb + woff, plo, phi, pk, wr);
         np += wr ? 1u : 0u;
         woff += (wr && woff < wlim) ? zstep : 0u;
         const bool take = closed && !drop_new;
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
         phi = take ? z : phi;
         pk = take ? kap : pk;
       } else {
-        st_pred_piece(zb + woff, kb + woff, zstart, z, kap, closed && has_out);
+        st_pred_piece(zb + woff, kb + woff, zstart, z, kap, closed);
         np += closed ? 1u : 0u;
         woff += (closed && woff < wlim) ? zstep : 0u;
       }
@@ -418,8 +419,13 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     }
   }
   };
-  if (staged) sweep(std::true_type{});
-  else sweep(std::false_type{});
+  if (staged) {
+    if (prune) sweep(std::true_type{}, std::true_type{});
+    else sweep(std::true_type{}, std::false_type{});
+  } else {
+    if (prune) sweep(std::false_type{}, std::true_type{});
+    else sweep(std::false_type{}, std::false_type{});
+  }
   if (use_ring) drain();
   if (prune && pk != KNONE) put(plo, phi, pk);
   if (!list_mode) {
