@@ -252,10 +252,12 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
 #define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
-  // small R: the ring-buffered emission variant (measured faster for R < 8, slower above)
+  // the ring-buffered emission variant (closed pieces parked in shared memory, filtered in
+  // batches) was faster for R < 8 until the inline filter became table-driven and branch-free;
+  // it is kept behind an experiment override (DEXEL_P1_RING_BELOW=R: use it below R)
   static const int ring_below = [] {
-    const char* e = std::getenv("DEXEL_P1_RING_BELOW");   // experiment override
-    return e ? std::atoi(e) : 8;
+    const char* e = std::getenv("DEXEL_P1_RING_BELOW");
+    return e ? std::atoi(e) : 0;
   }();
   if (R < ring_below && NW <= 2) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
   else if (NW <= 2) P1(2);
