@@ -84,7 +84,7 @@ __global__ void rebase_offsets(const uint64_t* __restrict__ src, uint64_t n, uin
 }
 
 // host-side diagnostics (DEXEL_DEBUG): seconds spent in allocation calls and stream syncs
-double g_t_alloc = 0.0, g_t_sync = 0.0;
+double g_t_alloc = 0.0, g_t_sync = 0.0, g_t_free = 0.0, g_t_info = 0.0;
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -131,6 +131,8 @@ dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
 
 void dfree(dexel_grid g, Buf& b) {
   if (!b.p) return;
+  const double t0 = now_s();
+  struct Acc { double t0; ~Acc() { g_t_free += now_s() - t0; } } acc_{t0};
   // free with the allocator that allocated it, even if the hook changed since
   if (b.freefn) b.freefn(b.p, b.bytes ? b.bytes : 16, g->d.device, (void*)g->stream, b.ctx);
   else cudaFreeAsync(b.p, g->stream);
@@ -541,7 +543,7 @@ void set_empty(dexel_grid g) {
 
 dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
   const double op_t0 = now_s();
-  g_t_alloc = g_t_sync = 0.0;
+  g_t_alloc = g_t_sync = g_t_free = g_t_info = 0.0;
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
   if (src == dst) return fail(DEXEL_EINVAL, "src and dst must be different handles");
   if (!same_geometry(src->d, dst->d)) return fail(DEXEL_EMISMATCH, "src and dst geometry differ");
@@ -622,10 +624,15 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   // slots of one band (pieces + level sets, all families): fewer, taller bands recompute fewer
   // halo rows (2R per band); the budget leaves room for the output staging and the caller
   size_t budget = (size_t)64 << 30;
-  {
+  // a grid whose whole extended slot set is small (under 1 GiB) is one band without asking the
+  // driver (cudaMemGetInfo costs 0.2-1.5 ms, a large share of a small op)
+  const size_t whole = row_bytes * (size_t)(src->nrows + 2 * Rmax);
+  if (whole > ((size_t)1 << 30)) {
     // free device memory plus what the stream-ordered pool holds but does not use (freed
     // temporaries of earlier ops stay reserved: the release threshold is kept at max)
     size_t fr = 0, tot = 0;
+    const double ti = now_s();
+    struct Acc { double t0; ~Acc() { g_t_info += now_s() - t0; } } acc_{ti};
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
       size_t pooled = 0;
       cudaMemPool_t pool;
@@ -730,8 +737,9 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   src->stats = stats;
   if (std::getenv("DEXEL_DEBUG")) {
     CK(timed_sync(st));
-    std::fprintf(stderr, "[dexel] op wall %.2f ms: allocation calls %.2f ms, stream syncs %.2f ms\n",
-                 1e3 * (now_s() - op_t0), 1e3 * g_t_alloc, 1e3 * g_t_sync);
+    std::fprintf(stderr, "[dexel] op wall %.2f ms: allocation calls %.2f ms, frees %.2f ms, memory queries %.2f ms, "
+                 "stream syncs %.2f ms\n", 1e3 * (now_s() - op_t0), 1e3 * g_t_alloc, 1e3 * g_t_free,
+                 1e3 * g_t_info, 1e3 * g_t_sync);
   }
   return DEXEL_OK;
 }

@@ -93,6 +93,17 @@ struct LvArgs {
 };
 
 constexpr int LV_T = 128;
+constexpr int LV_D = 8;      // pieces per thread in the cp.async ring
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // predicated 8-byte store without a branch (the compiler otherwise wraps each level's rare
 // emission in a BSSY/BRA/BSYNC region that some lane of the warp takes almost every step)
@@ -125,6 +136,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     const float h = (kap <= R && kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
     Hs[t] = h >= 0.f ? h : __int_as_float(0x7fc00000);   // quiet NaN
   }
+  __shared__ float2 ringz[LV_D][LV_T];
+  __shared__ uint32_t ringk[LV_D][LV_T];
   __syncthreads();
   uint32_t tot = 0, mx = 0;
   const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
@@ -174,19 +187,32 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs
     pce[k] = -INFINITY;   // no previous component
     o[k] = (uint32_t)k * olev;
   }
-  auto fetch = [&](int t, float2& z, int& kk) {
-    if (t < m) { z = zc[(int64_t)t * ps]; kk = kc[(int64_t)t * ps]; }
-    else { z = make_float2(0.f, 0.f); kk = L1; }
+  // pieces stream through a per-thread ring of LV_D shared-memory slots filled by cp.async
+  // (LV_D - 1 pieces in flight per thread, no registers held): z as 8 bytes, kappa as the
+  // aligned 4-byte word that holds it
+  auto issue = [&](int t) {
+    if (t < m) {
+      const int u = t % LV_D;
+      const uint8_t* kp = kc + (int64_t)t * ps;
+      cp_async8(&ringz[u][threadIdx.x], zc + (int64_t)t * ps);
+      cp_async4(&ringk[u][threadIdx.x], reinterpret_cast<const uint32_t*>((uintptr_t)kp & ~(uintptr_t)3));
+    }
+    cp_async_commit();   // (empty groups too: the wait count stays uniform)
   };
-  float2 nz, nz2;
-  int nk, nk2;
-  fetch(0, nz, nk);
-  fetch(1, nz2, nk2);
+#pragma unroll
+  for (int t = 0; t < LV_D - 1; ++t) issue(t);
   for (int t = 0; t < mmax; ++t) {
-    const float2 p = nz;
+    issue(t + LV_D - 1);
+    cp_async_wait<LV_D - 1>();        // piece t has landed (this thread's own copies)
+    float2 p = make_float2(0.f, 0.f);
+    int nk = L1;                      // past the column's pieces: the null piece
+    if (t < m) {
+      const int u = t % LV_D;
+      p = ringz[u][threadIdx.x];
+      const uintptr_t ka = (uintptr_t)(kc + (int64_t)t * ps);
+      nk = (int)((ringk[u][threadIdx.x] >> (8u * (uint32_t)(ka & 3))) & 0xffu);
+    }
     const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
-    nz = nz2; nk = nk2;
-    fetch(t + 2, nz2, nk2);
     float hv[4 * NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
