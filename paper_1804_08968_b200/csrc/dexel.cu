@@ -69,6 +69,9 @@ struct dexel_grid_s {
   unsigned char* pin = nullptr;   // pinned host scratch for the small device->host readbacks
   // capacity hints carried between ops (grown on overflow)
   int lev_cap = 0, p2_acc = 0, p1_cap = 0;
+  // device-memory budget for row bands, queried once and kept (a driver query per op costs
+  // 0.2-11 ms under contention, e.g. with a clock sampler); cleared when an op runs out of memory
+  size_t band_budget = 0;
   // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
   Buf hoff[2], hep[2];
   int hrows[2] = {0, 0};
@@ -541,7 +544,7 @@ void set_empty(dexel_grid g) {
   g->n = 0;
 }
 
-dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
+dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
   const double op_t0 = now_s();
   g_t_alloc = g_t_sync = g_t_free = g_t_info = 0.0;
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
@@ -627,7 +630,9 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   // a grid whose whole extended slot set is small (under 1 GiB) is one band without asking the
   // driver (cudaMemGetInfo costs 0.2-1.5 ms, a large share of a small op)
   const size_t whole = row_bytes * (size_t)(src->nrows + 2 * Rmax);
-  if (whole > ((size_t)1 << 30)) {
+  if (whole > ((size_t)1 << 30) && src->band_budget) {
+    budget = src->band_budget;
+  } else if (whole > ((size_t)1 << 30)) {
     // free device memory plus what the stream-ordered pool holds but does not use (freed
     // temporaries of earlier ops stay reserved: the release threshold is kept at max)
     size_t fr = 0, tot = 0;
@@ -644,6 +649,7 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
       }
       budget = std::min(budget, (fr + pooled) / 2);
     }
+    src->band_budget = budget;
   }
   int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
   if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override
@@ -742,6 +748,13 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
                  1e3 * g_t_info, 1e3 * g_t_sync);
   }
   return DEXEL_OK;
+}
+
+// an op that ran out of device memory drops the cached band budget (the next op re-queries)
+dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
+  const dexel_status s = run_op_impl(op, src, r_a, r_b, dst);
+  if (s == DEXEL_ENOMEM && src) src->band_budget = 0;
+  return s;
 }
 
 }  // namespace

@@ -1,5 +1,5 @@
 """Sum ncu --set full captures per kernel kind (one op's launches) -> profiles/traffic.json.
-usage: python tools/ncu_traffic.py report.ncu-rep KEY_PREFIX   (KEY_PREFIX e.g. C5:shell:16.0)
+usage: python tools/ncu_traffic.py report.ncu-rep|raw.csv KEY_PREFIX [traffic.json]   (KEY_PREFIX e.g. C5:shell:16.0)
 Kernel kinds follow bench.py: p1_kernel -> pass1, levels_kernel -> levels, pass2s -> pass2."""
 import csv
 import json
@@ -8,7 +8,8 @@ import subprocess
 import sys
 
 rep, prefix = sys.argv[1], sys.argv[2]
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+out = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rows = list(csv.reader(out.splitlines()))
 hdr, units = rows[0], rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
@@ -31,7 +32,8 @@ for r in rows[2:]:
     a["read"] += rd
     a["write"] += wr
     a["launches"] += 1
-path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
+path = sys.argv[3] if len(sys.argv) > 3 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                           "profiles", "traffic.json")
 tj = json.load(open(path)) if os.path.exists(path) else {}
 for kind, a in acc.items():
     tj[f"{prefix}:{kind}"] = a["read"] + a["write"]
