@@ -276,11 +276,10 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
 // Pass 1 over rows [row0, row0+nrows) of src: pieces into per-column slots (one launch);
 // columns with more than cap pieces are recomputed into an arena sized from the longest
 // column (a second, tile-list launch); too many of them doubles cap and reruns.
-dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
-                       PieceSlots* P, uint64_t* n_mid, const float* prune) {
+// p1_setup: the fixed per-band buffers; p1_slots: the slot arrays of one attempt (+ flag reset)
+dexel_status p1_setup(dexel_grid g, Temps& T, const SrcRows& src, int nrows, PieceSlots* P) {
   const int64_t ncol = (int64_t)nrows * src.nx;
   const int ntiles = (src.nx + 31) / 32;
-  const int NW = (32 + 2 * R + 31) / 32;
   dexel_status s;
   *P = PieceSlots{};
   P->nx = src.nx;
@@ -294,13 +293,64 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
   if ((s = T.get(sizeof(uint32_t) * P->ovf_list_cap * 2, (void**)&P->ovf_list))) return s;
   P->tile_list = P->ovf_list + P->ovf_list_cap;
   if ((s = T.get(sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), (void**)&P->tile_flag))) return s;
+  return DEXEL_OK;
+}
+
+dexel_status p1_slots(dexel_grid g, Temps& T, const SrcRows& src, int nrows, PieceSlots* P) {
+  const int64_t ncol = (int64_t)nrows * src.nx;
+  const int ntiles = (src.nx + 31) / 32;
+  dexel_status s;
+  const size_t nslot = (size_t)ncol * (P->cap + 1);
+  if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&P->z))) return s;
+  if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
+  CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
+  CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
+  CK(cudaMemsetAsync(P->ovf_idx, 0xff, sizeof(int32_t) * (ncol + 1), g->stream));   // -1: slots
+  return DEXEL_OK;
+}
+
+// after a main launch: hf = flags[0..2], tot = total.  Returns DEXEL_OK with *retry set when
+// too many columns overflowed (the caller doubles cap and reruns), else runs the list launch.
+dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
+                       PieceSlots* P, const unsigned* hf, unsigned long long tot, uint64_t* n_mid,
+                       const float* prune, bool* retry) {
+  const int NW = (32 + 2 * R + 31) / 32;
+  dexel_status s;
+  *retry = false;
+  if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
+    T.release(P->z);
+    T.release(P->k);
+    P->cap *= 2;
+    g->p1_cap = P->cap;
+    *retry = true;
+    return DEXEL_OK;
+  }
+  if (hf[0] > 0) {
+    P->ovf_cap = (int)hf[1];
+    const size_t na = (size_t)hf[0] * P->ovf_cap;
+    if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
+    if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
+    T.prof.pre(K_P1LIST);
+    launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], prune, g->stream);
+    T.prof.post();
+    CK(cudaGetLastError());
+    // the list launch adds the arena columns' (filtered) counts to the total
+    Readback rb{g};
+    rb.add(0, P->total, sizeof(tot));
+    CK(rb.wait());
+    rb.get(0, &tot, sizeof(tot));
+  }
+  *n_mid += tot;
+  return DEXEL_OK;
+}
+
+dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
+                       PieceSlots* P, uint64_t* n_mid, const float* prune) {
+  const int NW = (32 + 2 * R + 31) / 32;
+  dexel_status s;
+  if ((s = p1_setup(g, T, src, nrows, P))) return s;
   for (int attempt = 0; attempt < 8; ++attempt) {
-    const size_t nslot = (size_t)ncol * (P->cap + 1);
-    if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&P->z))) return s;
-    if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
-    CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
-    CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
-    CK(cudaMemsetAsync(P->ovf_idx, 0xff, sizeof(int32_t) * (ncol + 1), g->stream));   // -1: slots
+    if ((s = p1_slots(g, T, src, nrows, P))) return s;
     T.prof.pre(K_P1);
     launch_p1(NW, src, R, complement, row0, nrows, *P, -1, prune, g->stream);
     T.prof.post();
@@ -315,32 +365,55 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
       rb.get(0, hf, sizeof(hf));
       rb.get(16, &tot, sizeof(tot));
     }
-    if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
-      T.release(P->z);
-      T.release(P->k);
-      P->cap *= 2;
-      g->p1_cap = P->cap;
-      continue;
-    }
-    if (hf[0] > 0) {
-      P->ovf_cap = (int)hf[1];
-      const size_t na = (size_t)hf[0] * P->ovf_cap;
-      if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
-      if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
-      T.prof.pre(K_P1LIST);
-      launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], prune, g->stream);
-      T.prof.post();
-      CK(cudaGetLastError());
-      // the list launch adds the arena columns' (filtered) counts to the total
-      Readback rb{g};
-      rb.add(0, P->total, sizeof(tot));
-      CK(rb.wait());
-      rb.get(0, &tot, sizeof(tot));
-    }
-    *n_mid += tot;
-    return DEXEL_OK;
+    bool retry = false;
+    if ((s = p1_finish(g, T, src, R, complement, row0, nrows, P, hf, tot, n_mid, prune, &retry))) return s;
+    if (!retry) return DEXEL_OK;
   }
   return fail(DEXEL_ECUDA, "pass-1 slot sizing did not converge");
+}
+
+// both shell families (S at r_a, C = U \ S at r_b, the same R <= 16) in one sweep
+// (p1_dual_kernel); a family whose slots overflow too often is redone alone by run_pass1
+dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, int row0, int nrows,
+                            PieceSlots* PA, PieceSlots* PB, uint64_t* n_mid, const float* prune_a,
+                            const float* prune_b) {
+  dexel_status s;
+  if ((s = p1_setup(g, T, src, nrows, PA))) return s;
+  if ((s = p1_setup(g, T, src, nrows, PB))) return s;
+  if ((s = p1_slots(g, T, src, nrows, PA))) return s;
+  if ((s = p1_slots(g, T, src, nrows, PB))) return s;
+  const int64_t warps = (int64_t)nrows * ((src.nx + 31) / 32);
+  const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
+  if (blocks > 0) {
+    T.prof.pre(K_P1);
+    p1_dual_kernel<<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
+    T.prof.post();
+    CK(cudaGetLastError());
+  }
+  unsigned hf[2][4];
+  unsigned long long tot[2] = {0, 0};
+  {
+    Readback rb{g};
+    rb.add(0, PA->flags, 3 * sizeof(unsigned));
+    rb.add(16, PA->total, sizeof(tot[0]));
+    rb.add(32, PB->flags, 3 * sizeof(unsigned));
+    rb.add(48, PB->total, sizeof(tot[1]));
+    CK(rb.wait());
+    rb.get(0, hf[0], 3 * sizeof(unsigned));
+    rb.get(16, &tot[0], sizeof(tot[0]));
+    rb.get(32, hf[1], 3 * sizeof(unsigned));
+    rb.get(48, &tot[1], sizeof(tot[1]));
+  }
+  for (int f = 0; f < 2; ++f) {
+    PieceSlots* P = f ? PB : PA;
+    const float* prune = f ? prune_b : prune_a;
+    bool retry = false;
+    if ((s = p1_finish(g, T, src, R, f, row0, nrows, P, hf[f], tot[f], n_mid, prune, &retry))) return s;
+    if (retry) {   // rare: this family alone, with grown slots
+      if ((s = run_pass1(g, T, src, R, f, row0, nrows, P, n_mid, prune))) return s;
+    }
+  }
+  return DEXEL_OK;
 }
 
 void release_pieces(Temps& T, PieceSlots& P) {
@@ -380,11 +453,14 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
 // level slots of one family for level rows [lr0, lr0 + lrn) (extended-row numbering):
 // pass 1 on those rows, then the level-set kernel; the pieces are freed on return.
 // A level list longer than the slot capacity reruns the level kernel with a larger cap.
+// (pre != nullptr: the family's pieces were computed already, by run_pass1_dual)
 dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, const float* prune,
-                        int complement, int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev) {
+                        int complement, int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev,
+                        const PieceSlots* pre = nullptr) {
   dexel_status s;
   PieceSlots P;
-  if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid, prune))) return s;
+  if (pre) P = *pre;
+  else if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid, prune))) return s;
   const int64_t ncol = (int64_t)lrn * src.nx;
   unsigned* flags = nullptr;
   if ((s = T.get(64, (void**)&flags))) return s;
@@ -617,9 +693,14 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   const int nx = src->d.nx;
   const int nfam = op == OP_SHELL ? 2 : 1;
   int lcap = src->lev_cap > 0 ? src->lev_cap : 8;
-  // bytes per level row of a band: level slots of all families + one family's piece slots
+  // the shell's two pass-1 families in one sweep (p1_dual_kernel) when they share R <= 16 and
+  // both filter (DEXEL_NO_FUSE=1 runs them separately, for testing)
+  static const bool no_fuse = [] { const char* e = std::getenv("DEXEL_NO_FUSE"); return e && std::atoi(e); }();
+  const bool fused = op == OP_SHELL && Ra == Rb && Ra <= 16 && prune_a && prune_b && !no_fuse;
+  // bytes per level row of a band: level slots of all families + the piece slots alive at once
+  // (one family's, or both when fused)
   const int pcap = src->p1_cap > 0 ? src->p1_cap : 256;
-  size_t row_bytes = (size_t)nx * ((size_t)(pcap + 1) * (sizeof(float2) + 1) + 8);
+  size_t row_bytes = (size_t)nx * ((size_t)(pcap + 1) * (sizeof(float2) + 1) + 8) * (fused ? 2 : 1);
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
     row_bytes += (size_t)nx * ((Rf + 1) * sizeof(uint16_t) + (Rf + 2) * sizeof(float2) * (size_t)(lcap + 1));
@@ -654,6 +735,10 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
   if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override
   band = std::min(band, src->nrows);
+  {   // equal bands: every band's slot arrays then fit the blocks the first band allocated
+    const int nb = (src->nrows + band - 1) / band;
+    band = (src->nrows + nb - 1) / nb;
+  }
   stats.lev_cap = 0;
   uint32_t* ocnt = nullptr;
   unsigned* flags = nullptr;
@@ -670,14 +755,20 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       const int b1 = std::min(src->nrows, b0 + band);
       const int lr0 = std::max(0, hlo + b0 - Rmax), lr1 = std::min(nrows_ext, hlo + b1 + Rmax);
       LevelSlots LA{}, LB{};
+      PieceSlots PA{}, PB{};
+      if (fused && (s = run_pass1_dual(src, T, rows, Ra, lr0, lr1 - lr0, &PA, &PB, &stats.n_mid, prune_a, prune_b))) {
+        set_empty(dst);
+        return s;
+      }
       // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
       if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
-                          &stats.n_lev))) {
+                          &stats.n_lev, fused ? &PA : nullptr))) {
         set_empty(dst);
         return s;
       }
       if (op == OP_SHELL) {
-        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev))) {
+        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev,
+                            fused ? &PB : nullptr))) {
           set_empty(dst);
           return s;
         }

@@ -452,6 +452,217 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   }
 }
 
+// ------------------------------------------------------------------ pass 1, both shell families
+// The shell needs pass 1 of S (r_out) and of C = U \ S (r_in).  When both radii give the same
+// R <= 16 one sweep serves both: C's endpoints are S's (plus z_lo / z_hi), so the window events
+// are the same, and between two events a window column is in C exactly when it is in the grid
+// and not in S -- C's activity mask is G & ~M (G = the window's in-grid columns).  C's pieces
+// start at z_lo (before the first event every in-grid column is in C) and its last piece
+// closes at z_hi; zero-length C pieces (an S interval starting at z_lo or ending at z_hi) are
+// dropped, exactly as complement-on-load drops them (col_open).  The unfiltered piece sequence
+// of each family is therefore the one its own sweep produces, and so are the filtered pieces.
+// The event half of a sweep step (REDUX, ballots, key advance) and the key staging run once
+// for both families.  Main pass only (overflow columns are redone per family in list mode).
+
+// capsule-domination thresholds of every (pending kappa, new kappa) pair (see p1_kernel)
+__device__ __forceinline__ void p1_thr_init(float2* thr, const float* __restrict__ prune, int R) {
+  for (int t = threadIdx.x; t < 18 * 32; t += blockDim.x) {
+    const int kp = t >> 5, kn = t & 31;
+    float2 v = make_float2(-INFINITY, -INFINITY);
+    if (kp <= R && kn <= R) {
+      const float D = prune[kp] - prune[kn];                // H[kp] - H[kn]
+      if (kp <= kn) v.x = D - 1e-6f * (1.0f + fabsf(D));    // drop new:     hi_n - hi_p <= x
+      if (kn <= kp) v.y = -D - 1e-6f * (1.0f + fabsf(D));   // drop pending: lo_n - lo_p <= y
+    }
+    thr[t] = v;
+  }
+}
+
+// one family's output state in the dual sweep
+struct P1Fam {
+  float2* zb;
+  uint8_t* kb;
+  uint32_t zstep, woff, wlim, np;
+  bool has_out;
+  float plo, phi;   // pending piece of the domination filter
+  int pk;
+};
+
+__device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int jr, int i, bool out_ok) {
+  // lanes without output store into a spill cell (slot cap, never read)
+  F.zb = P.z + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
+  F.kb = P.k + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
+  F.zstep = out_ok ? (uint32_t)P.nx : 0u;
+  F.wlim = (uint32_t)P.cap * F.zstep;   // the spill cell
+  F.woff = 0;
+  F.np = 0;
+  F.has_out = out_ok;
+  F.plo = F.phi = 0.f;
+  F.pk = KNONE;
+}
+
+// a piece [zstart, z] at level kap closed (closed == true): the domination filter against the
+// pending piece, branch-free (the p1_kernel inline path with the threshold table)
+__device__ __forceinline__ void p1_fam_step(P1Fam& F, bool closed, float zstart, float z, int kap,
+                                            const float2* thr) {
+  const bool hp = F.pk != KNONE;
+  const float2 th = thr[min(F.pk, 17) * 32 + (kap & 31)];
+  const bool drop_new = z - F.phi <= th.x;
+  const bool drop_pend = zstart - F.plo <= th.y;
+  const bool wr = closed && hp && !drop_new && !drop_pend;
+  st_pred_piece(F.zb + F.woff, F.kb + F.woff, F.plo, F.phi, F.pk, wr);
+  F.np += wr ? 1u : 0u;
+  F.woff += (wr && F.woff < F.wlim) ? F.zstep : 0u;
+  const bool take = closed && !drop_new;
+  F.plo = take ? zstart : F.plo;
+  F.phi = take ? z : F.phi;
+  F.pk = take ? kap : F.pk;
+}
+
+// flush the pending piece, store the count, list an overflowing column for list mode
+__device__ __forceinline__ void p1_fam_finish(P1Fam& F, PieceSlots& P, int64_t c, int jr, int tile, int ntiles) {
+  if (F.has_out && F.pk != KNONE) {
+    const uint32_t t = min(F.np, (uint32_t)P.cap);
+    F.zb[(size_t)t * F.zstep] = make_float2(F.plo, F.phi);
+    F.kb[(size_t)t * F.zstep] = (uint8_t)F.pk;
+    ++F.np;
+  }
+  if (F.has_out) {
+    P.cnt[c] = F.np;
+    if (F.np > (uint32_t)P.cap) {
+      atomicMax(P.flags + 1, F.np);
+      const unsigned slot = atomicAdd(P.flags, 1u);
+      if (slot < P.ovf_list_cap) {
+        P.ovf_idx[c] = (int32_t)slot;
+        const size_t tf = (size_t)jr * ntiles + tile;
+        if (atomicExch(P.tile_flag + tf, 1u) == 0u) {
+          const unsigned ts = atomicAdd(P.flags + 2, 1u);
+          P.tile_list[ts] = (uint32_t)tf;
+        }
+      }
+    }
+  }
+  const unsigned wsum = __reduce_add_sync(FULL, (F.has_out && F.np <= (uint32_t)P.cap) ? F.np : 0u);
+  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(P.total, (unsigned long long)wsum);
+}
+
+__global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int R, int row0, int nrows_out,
+                                                                 PieceSlots PS, PieceSlots PC,
+                                                                 const float* __restrict__ prune_s,
+                                                                 const float* __restrict__ prune_c) {
+  __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
+  __shared__ float2 thr_s[18 * 32], thr_c[18 * 32];
+  p1_thr_init(thr_s, prune_s, R);
+  p1_thr_init(thr_c, prune_c, R);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t* stage = stage_all[threadIdx.x >> 5];
+  const int ntiles = (src.nx + 31) >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= (int64_t)nrows_out * ntiles) return;  // warp-uniform
+  const int jr = (int)(gw / ntiles), tile = (int)(gw % ntiles);
+  const int j = row0 + jr;
+  const int i0 = tile * 32;
+  const int W = 32 + 2 * R;
+  constexpr int NW = 2;
+
+  // the window's S endpoints as keys (as p1_kernel with complement = 0)
+  ColCursor cur[NW];
+  uint32_t sb[NW], pos[NW], end[NW], nkey[NW], G[NW];
+  uint32_t total = 0;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    const int w = lane + 32 * q;
+    const int gi = i0 - R + w;
+    G[q] = __ballot_sync(FULL, w < W && gi >= 0 && gi < src.nx);   // in-grid window columns
+    if (w < W) col_open(src, gi, j, 0, cur[q]);
+    else { cur[q].base = 0; cur[q].n = 0; cur[q].v = 0; cur[q].vend = 0; }
+    const uint32_t nv = cur[q].vend - cur[q].v + 1;
+    uint32_t incl = nv;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    sb[q] = total + incl - nv;
+    total += __shfl_sync(FULL, incl, 31);
+  }
+  const bool staged = total <= (uint32_t)P1_STAGE;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    const uint32_t nv = cur[q].vend - cur[q].v;
+    if (staged) {
+      for (uint32_t t = 0; t < nv; ++t) stage[sb[q] + t] = fkey(col_value(src, cur[q], cur[q].v + t, 0));
+      stage[sb[q] + nv] = KEY_NONE;
+      pos[q] = sb[q];
+      end[q] = sb[q] + nv;
+    } else {
+      pos[q] = cur[q].v;
+      end[q] = cur[q].vend;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < NW; ++q)
+    nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(col_value(src, cur[q], pos[q], 0))) : KEY_NONE;
+
+  const int i = i0 + lane;
+  const bool out_ok = i < src.nx;
+  const int64_t c = (int64_t)jr * src.nx + i;
+  P1Fam FS, FC;
+  p1_fam_init(FS, PS, jr, i, out_ok);
+  p1_fam_init(FC, PC, jr, i, out_ok);
+  const int pp = lane + R;
+  const int shr = pp < 32 ? pp : pp - 32;
+  const int shl = pp >= 31 ? pp - 31 : 31 - pp;
+  const bool rlow = pp < 32, lhigh = pp >= 31;
+  auto nearest2 = [&](uint32_t m0, uint32_t m1) -> int {
+    const uint32_t rw = __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr) | 0x80000000u;
+    const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
+    const uint32_t lw = (lhigh ? la : lb) | 1u;
+    const int d = min(__clz(lw), __ffs(rw) - 1);
+    return d <= R ? d : KNONE;
+  };
+  uint32_t M0 = 0u, M1 = 0u;                   // S activity of the window (warp-uniform)
+  int kap = KNONE, kapc = nearest2(G[0], G[1]);
+  float zstart = 0.f, zstartc = src.zlo;
+  auto sweep = [&](auto stg) {
+    for (;;) {
+      const uint32_t zk = __reduce_min_sync(FULL, min(nkey[0], nkey[1]));
+      if (zk == KEY_NONE) break;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        const bool hit = nkey[q] == zk;
+        const uint32_t b = __ballot_sync(FULL, hit);
+        if (q == 0) M0 ^= b; else M1 ^= b;
+        if constexpr (decltype(stg)::value) {
+          pos[q] += hit ? 1u : 0u;
+          if (hit) nkey[q] = stage[pos[q]];
+        } else if (hit) {
+          ++pos[q];
+          nkey[q] = pos[q] < end[q] ? fkey(col_value(src, cur[q], pos[q], 0)) : KEY_NONE;
+        }
+      }
+      const float z = keyf(zk);
+      const int knew = nearest2(M0, M1);
+      const int knewc = nearest2(G[0] & ~M0, G[1] & ~M1);
+      const bool chg = knew != kap, chgc = knewc != kapc;
+      p1_fam_step(FS, chg && kap != KNONE, zstart, z, kap, thr_s);
+      p1_fam_step(FC, chgc && kapc != KNONE && zstartc < z, zstartc, z, kapc, thr_c);
+      kap = chg ? knew : kap;
+      zstart = chg ? z : zstart;
+      kapc = chgc ? knewc : kapc;
+      zstartc = chgc ? z : zstartc;
+    }
+  };
+  if (staged) sweep(std::true_type{});
+  else sweep(std::false_type{});
+  // C's last piece closes at z_hi
+  p1_fam_step(FC, kapc != KNONE && zstartc < src.zhi, zstartc, src.zhi, kapc, thr_c);
+  p1_fam_finish(FS, PS, c, jr, tile, ntiles);
+  p1_fam_finish(FC, PC, c, jr, tile, ntiles);
+}
+
 // pieces of a band (slots + arena) -> CSR (dexel_pass1, parity testing only)
 __global__ void pieces_to_csr(PieceSlots P, int64_t ncol, const uint64_t* __restrict__ off, float2* __restrict__ oz,
                               uint8_t* __restrict__ ok) {

@@ -361,6 +361,52 @@ print("OK")
     assert all(a < b for a, b in zip(mids["0"], mids["1"])), mids
 
 
+@pytest.mark.parametrize("p1cap", [None, "3"])
+def test_fused_shell_pass1_is_bitwise_separate(dx, p1cap):
+    """The shell's two pass-1 families in one sweep (p1_dual_kernel, used when r_out and r_in
+    share R <= 16) give bitwise the output of two separate sweeps (DEXEL_NO_FUSE=1), and match
+    the oracle -- also with tiny pass-1 slots (overflow columns redone per family in list mode),
+    with S touching z_lo / z_hi (zero-length complement pieces) and with r_out != r_in."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, hashlib; sys.path.insert(0, %r)
+import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
+from oracle.compare import compare
+cases = [("C2", G.config("C2"), 4.0, 4.0), ("C2", G.config("C2"), 6.5, 6.2), ("C1", G.config("C1"), 3.0, 3.0)]
+rng = np.random.default_rng(7)
+cols = []
+for c in range(40 * 24):          # columns touching the domain ends
+    k = int(rng.integers(0, 4)); pts = np.sort(rng.uniform(-8, 8, 2 * k)).astype(np.float32)
+    iv = [(float(pts[2*t]), float(pts[2*t+1])) for t in range(k) if pts[2*t] < pts[2*t+1]]
+    if c %% 3 == 0: iv = [(-8.0, -7.0)] + [x for x in iv if x[0] > -7.0]
+    if c %% 5 == 0: iv = [x for x in iv if x[1] < 7.5] + [(7.5, 8.0)]
+    cols.append(iv)
+cases.append(("edge", G.from_columns(40, 24, cols, -8.0, 8.0), 5.0, 5.0))
+h = hashlib.sha256()
+for name, host, ro, ri in cases:
+    src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
+    dx.dexel_shell(src, ro, ri, dst)
+    off, ep = dst.download()
+    h.update(np.asarray(off).tobytes()); h.update(np.asarray(ep).tobytes())
+    ref = O.shell(host, ro, ri)
+    res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (name, ro, ri, res)
+print("HASH", h.hexdigest())
+print("OK")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hashes = {}
+    for fuse in ("0", "1"):
+        env = dict(os.environ, DEXEL_NO_FUSE=fuse)
+        if p1cap:
+            env["DEXEL_P1_CAP"] = p1cap
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+        hashes[fuse] = [l for l in out.stdout.splitlines() if l.startswith("HASH")][0]
+    assert hashes["0"] == hashes["1"], hashes
+
+
 # ---------------------------------------------------------------- openings / closings (NEXT #1)
 def _to_host_grid(host, res):
     """an oracle Result as an fp32 canonical input grid (touching after rounding: merged)."""
