@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     const int d = min(__clz(lw), __ffs(rw) - 1);
     return d <= R ? d : KNONE;
   };
+  const bool skip_ok = R >= 8;   // skipping steps no lane changes pays from R = 8 (measured)
   // the sweep, versioned on the (warp-uniform) staging decision so the hot loop carries no
   // global-memory fallback
   auto sweep = [&](auto stg, auto prn) {
@@ -385,6 +386,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       if (__any_sync(FULL, rc - rd == (uint32_t)P1_RING)) drain();
     } else {                                 // inline filter, branch-free (measured faster for larger R)
       const bool chg = knew != kap;
+      // an event changes kappa only for lanes within R of its column: steps where no lane of
+      // the warp changes (often: halo events) skip the filter / emission half (warp-uniform)
+      if (skip_ok && !__any_sync(FULL, chg)) continue;
       const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
       if constexpr (decltype(prn)::value) {   // (the sweep is versioned on prune != nullptr)
@@ -624,6 +628,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
     return d <= R ? d : KNONE;
   };
   uint32_t M0 = 0u, M1 = 0u;                   // S activity of the window (warp-uniform)
+  const bool skip_ok = R >= 8;                 // (for small R almost every step changes a lane)
   int kap = KNONE, kapc = nearest2(G[0], G[1]);
   float zstart = 0.f, zstartc = src.zlo;
   auto sweep = [&](auto stg) {
@@ -647,12 +652,18 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
       const int knew = nearest2(M0, M1);
       const int knewc = nearest2(G[0] & ~M0, G[1] & ~M1);
       const bool chg = knew != kap, chgc = knewc != kapc;
-      p1_fam_step(FS, chg && kap != KNONE, zstart, z, kap, thr_s);
-      p1_fam_step(FC, chgc && kapc != KNONE && zstartc < z, zstartc, z, kapc, thr_c);
-      kap = chg ? knew : kap;
-      zstart = chg ? z : zstart;
-      kapc = chgc ? knewc : kapc;
-      zstartc = chgc ? z : zstartc;
+      // an event changes kappa only for lanes within R of its column: steps where no lane of
+      // the warp changes (often: halo events) skip the filter / emission half (warp-uniform)
+      if (!skip_ok || __any_sync(FULL, chg)) {
+        p1_fam_step(FS, chg && kap != KNONE, zstart, z, kap, thr_s);
+        kap = chg ? knew : kap;
+        zstart = chg ? z : zstart;
+      }
+      if (!skip_ok || __any_sync(FULL, chgc)) {
+        p1_fam_step(FC, chgc && kapc != KNONE && zstartc < z, zstartc, z, kapc, thr_c);
+        kapc = chgc ? knewc : kapc;
+        zstartc = chgc ? z : zstartc;
+      }
     }
   };
   if (staged) sweep(std::true_type{});
