@@ -257,6 +257,7 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
 #define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
+  // (skipping sweep steps that change no lane's kappa pays from R = 8; measured)
   // the ring-buffered emission variant (closed pieces parked in shared memory, filtered in
   // batches) was faster for R < 8 until the inline filter became table-driven and branch-free;
   // it is kept behind an experiment override (DEXEL_P1_RING_BELOW=R: use it below R)
@@ -265,6 +266,8 @@ void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int 
     return e ? std::atoi(e) : 0;
   }();
   if (R < ring_below && NW <= 2) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
+  else if (NW <= 2 && R < 8)
+    p1_kernel<2, false, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
   else if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);
@@ -386,7 +389,8 @@ dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, i
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks > 0) {
     T.prof.pre(K_P1);
-    p1_dual_kernel<<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
+    if (R >= 8) p1_dual_kernel<true><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
+    else p1_dual_kernel<false><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
     T.prof.post();
     CK(cudaGetLastError());
   }

@@ -182,7 +182,8 @@ __device__ __forceinline__ bool dom_margin(float lhs, float rhs) {
   return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs));
 }
 
-template <int NW, bool RING>
+// SKIP (host: R >= 8): steps where no lane's kappa changes skip the filter / emission half
+template <int NW, bool RING, bool SKIP = true>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, int complement, int row0,
                                                             int nrows_out, PieceSlots P, int64_t nlist,
                                                             const float* __restrict__ prune) {
@@ -347,7 +348,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
     const int d = min(__clz(lw), __ffs(rw) - 1);
     return d <= R ? d : KNONE;
   };
-  const bool skip_ok = R >= 8;   // skipping steps no lane changes pays from R = 8 (measured)
   // the sweep, versioned on the (warp-uniform) staging decision so the hot loop carries no
   // global-memory fallback
   auto sweep = [&](auto stg, auto prn) {
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       const bool chg = knew != kap;
       // an event changes kappa only for lanes within R of its column: steps where no lane of
       // the warp changes (often: halo events) skip the filter / emission half (warp-uniform)
-      if (skip_ok && !__any_sync(FULL, chg)) continue;
+      if (SKIP && !__any_sync(FULL, chg)) continue;
       const bool closed = chg && kap != KNONE;
       const float z = keyf(zk);
       if constexpr (decltype(prn)::value) {   // (the sweep is versioned on prune != nullptr)
@@ -550,6 +550,7 @@ __device__ __forceinline__ void p1_fam_finish(P1Fam& F, PieceSlots& P, int64_t c
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(P.total, (unsigned long long)wsum);
 }
 
+template <bool SKIP>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int R, int row0, int nrows_out,
                                                                  PieceSlots PS, PieceSlots PC,
                                                                  const float* __restrict__ prune_s,
@@ -628,7 +629,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
     return d <= R ? d : KNONE;
   };
   uint32_t M0 = 0u, M1 = 0u;                   // S activity of the window (warp-uniform)
-  const bool skip_ok = R >= 8;                 // (for small R almost every step changes a lane)
   int kap = KNONE, kapc = nearest2(G[0], G[1]);
   float zstart = 0.f, zstartc = src.zlo;
   auto sweep = [&](auto stg) {
@@ -654,12 +654,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
       const bool chg = knew != kap, chgc = knewc != kapc;
       // an event changes kappa only for lanes within R of its column: steps where no lane of
       // the warp changes (often: halo events) skip the filter / emission half (warp-uniform)
-      if (!skip_ok || __any_sync(FULL, chg)) {
+      if (!SKIP || __any_sync(FULL, chg)) {
         p1_fam_step(FS, chg && kap != KNONE, zstart, z, kap, thr_s);
         kap = chg ? knew : kap;
         zstart = chg ? z : zstart;
       }
-      if (!skip_ok || __any_sync(FULL, chgc)) {
+      if (!SKIP || __any_sync(FULL, chgc)) {
         p1_fam_step(FC, chgc && kapc != KNONE && zstartc < z, zstartc, z, kapc, thr_c);
         kapc = chgc ? knewc : kapc;
         zstartc = chgc ? z : zstartc;
