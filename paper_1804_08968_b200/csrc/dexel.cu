@@ -72,6 +72,16 @@ struct dexel_grid_s {
   // device-memory budget for row bands, queried once and kept (a driver query per op costs
   // 0.2-11 ms under contention, e.g. with a clock sampler); cleared when an op runs out of memory
   size_t band_budget = 0;
+  // workspace: an op's large temporaries (band slot arrays, staging) stay allocated on the
+  // handle and are reused by size by later ops; freeing them to the stream-ordered pool and
+  // allocating again fragments the pool once other allocations (e.g. a re-upload) land in
+  // the freed blocks, and the pool then remaps tens of GB per op (measured: 150-900 ms)
+  std::vector<Buf> ws;
+  std::vector<char> ws_busy;
+  size_t ws_bytes = 0;
+  // the previous input CSR after a re-upload: the next upload of a similar size fills it
+  // instead of allocating (an upload must not touch the current contents until validated)
+  Buf spare_off, spare_ep;
   // y-slab halos (multi-GPU): rows [y0 - hrows[0], y0) and [y1, y1 + hrows[1]) of the input
   Buf hoff[2], hep[2];
   int hrows[2] = {0, 0};
@@ -183,9 +193,12 @@ struct Prof {
 };
 
 // RAII for temporaries of one op
+constexpr size_t WS_MIN = (size_t)32 << 20;   // temporaries from this size on use the workspace
+
 struct Temps {
   dexel_grid g;
   std::vector<Buf> bufs;
+  std::vector<int> wsi;   // workspace entries this op holds
   Prof prof;
   explicit Temps(dexel_grid g_, dexel_stats* st = nullptr) : g(g_) {
     prof.st = g_->stream;
@@ -195,8 +208,34 @@ struct Temps {
   ~Temps() {
     prof.finish();
     for (auto& b : bufs) dfree(g, b);
+    for (int w : wsi) g->ws_busy[w] = 0;
   }
   dexel_status get(size_t bytes, void** p) {
+    if (bytes >= WS_MIN) {   // a free workspace block of about this size (at most 1/4 larger)
+      int best = -1;
+      for (int w = 0; w < (int)g->ws.size(); ++w)
+        if (!g->ws_busy[w] && g->ws[w].bytes >= bytes && g->ws[w].bytes - bytes <= bytes / 4 &&
+            (best < 0 || g->ws[w].bytes < g->ws[best].bytes))
+          best = w;
+      if (best < 0) {
+        Buf b;
+        dexel_status s = dalloc(g, b, bytes);
+        if (s == DEXEL_ENOMEM) {   // drop the idle workspace and retry once
+          trim_idle();
+          g_err.clear();
+          s = dalloc(g, b, bytes);
+        }
+        if (s) return s;
+        g->ws.push_back(b);
+        g->ws_busy.push_back(0);
+        g->ws_bytes += b.bytes;
+        best = (int)g->ws.size() - 1;
+      }
+      g->ws_busy[best] = 1;
+      wsi.push_back(best);
+      *p = g->ws[best].p;
+      return DEXEL_OK;
+    }
     Buf b;
     dexel_status s = dalloc(g, b, bytes);
     if (s) return s;
@@ -207,6 +246,20 @@ struct Temps {
   void release(void* p) {
     for (auto& b : bufs)
       if (b.p == p) dfree(g, b);
+    for (size_t t = 0; t < wsi.size(); ++t)
+      if (g->ws[wsi[t]].p == p) {
+        g->ws_busy[wsi[t]] = 0;
+        wsi.erase(wsi.begin() + t);
+        break;
+      }
+  }
+  // free the workspace blocks no op holds (their slots stay in the vector as empty entries)
+  void trim_idle() {
+    for (size_t w = 0; w < g->ws.size(); ++w)
+      if (!g->ws_busy[w] && g->ws[w].p) {
+        g->ws_bytes -= g->ws[w].bytes;
+        dfree(g, g->ws[w]);
+      }
   }
 };
 
@@ -818,8 +871,13 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   uint64_t nout = 0;
   if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
   if ((s = scan_counts(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p, &nout))) return s;
-  dfree(dst, dst->ep);
-  if ((s = dalloc(dst, dst->ep, sizeof(float2) * (nout + 1)))) return s;
+  {   // the output endpoints: the current buffer is reused when the size fits (dst != src)
+    const size_t need = sizeof(float2) * (nout + 1);
+    if (!(dst->ep.p && dst->ep.bytes >= need && dst->ep.bytes - need <= need / 4)) {
+      dfree(dst, dst->ep);
+      if ((s = dalloc(dst, dst->ep, need))) return s;
+    }
+  }
   if (ncol > 0)
     LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(
                              stage, ocnt, (const uint64_t*)dst->off.p, ncol, (float2*)dst->ep.p));
@@ -928,8 +986,18 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
 
 namespace {
 // copy + validate a CSR of ncol columns into fresh buffers (grid unchanged on error)
+// b := the spare buffer if it holds bytes (and at most 1/4 more), else a new allocation
+dexel_status take_or_alloc(dexel_grid g, Buf* spare, Buf& b, size_t bytes) {
+  if (spare && spare->p && spare->bytes >= bytes && spare->bytes - bytes <= bytes / 4) {
+    b = *spare;
+    *spare = Buf{};
+    return DEXEL_OK;
+  }
+  return dalloc(g, b, bytes);
+}
+
 dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoints, int64_t ncol, uint64_t n,
-                      int on_dev, Buf* off_out, Buf* ep_out) {
+                      int on_dev, Buf* off_out, Buf* ep_out, Buf* spare_off = nullptr, Buf* spare_ep = nullptr) {
   if (!offsets || (n > 0 && !endpoints)) return fail(DEXEL_EINVAL, "NULL argument");
   CK(cudaSetDevice(g->d.device));
   uint64_t first = 0, last = 0;
@@ -944,8 +1012,8 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
   if (first != 0 || last != n) return fail(DEXEL_EINVAL, "offsets[0] must be 0 and offsets[ncols] == n_intervals");
   Buf off, ep;
   dexel_status s;
-  if ((s = dalloc(g, off, sizeof(uint64_t) * (ncol + 1)))) return s;
-  if ((s = dalloc(g, ep, sizeof(float) * 2 * (n + 1)))) {
+  if ((s = take_or_alloc(g, spare_off, off, sizeof(uint64_t) * (ncol + 1)))) return s;
+  if ((s = take_or_alloc(g, spare_ep, ep, sizeof(float) * 2 * (n + 1)))) {
     dfree(g, off);
     return s;
   }
@@ -987,11 +1055,20 @@ extern "C" {
 dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev) {
   g_err.clear();
   if (!g) return fail(DEXEL_EINVAL, "NULL handle");
+  static const bool dbg = std::getenv("DEXEL_DEBUG") != nullptr;
+  const double t0 = now_s();
+  g_t_alloc = g_t_sync = 0.0;
   Buf off, ep;
-  dexel_status s = load_csr(g, offsets, endpoints, g->ncol, n, on_dev, &off, &ep);
+  dexel_status s = load_csr(g, offsets, endpoints, g->ncol, n, on_dev, &off, &ep, &g->spare_off, &g->spare_ep);
   if (s) return s;
-  dfree(g, g->off);
-  dfree(g, g->ep);
+  if (dbg)
+    std::fprintf(stderr, "[dexel] upload %llu intervals: %.2f ms (allocation calls %.2f ms, stream syncs %.2f ms)\n",
+                 (unsigned long long)n, 1e3 * (now_s() - t0), 1e3 * g_t_alloc, 1e3 * g_t_sync);
+  // the previous contents become the spare (a larger spare from before is released)
+  dfree(g, g->spare_off);
+  dfree(g, g->spare_ep);
+  g->spare_off = g->off;
+  g->spare_ep = g->ep;
   g->off = off;
   g->ep = ep;
   g->n = n;
@@ -1123,9 +1200,13 @@ dexel_status dexel_download(dexel_grid g, uint64_t* offsets, float* endpoints, u
   if (cap < g->n) return fail(DEXEL_EOVERFLOW, "capacity " + std::to_string(cap) + " < " + std::to_string(g->n));
   CK(cudaSetDevice(g->d.device));
   const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const double t0 = now_s();
   CK(cudaMemcpyAsync(offsets, g->off.p, sizeof(uint64_t) * (g->ncol + 1), k, g->stream));
   if (g->n) CK(cudaMemcpyAsync(endpoints, g->ep.p, sizeof(float) * 2 * g->n, k, g->stream));
   CK(timed_sync(g->stream));
+  static const bool dbg = std::getenv("DEXEL_DEBUG") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "[dexel] download %llu intervals: %.2f ms\n", (unsigned long long)g->n, 1e3 * (now_s() - t0));
   return DEXEL_OK;
 }
 
@@ -1183,6 +1264,9 @@ void dexel_destroy(dexel_grid g) {
     dfree(g, g->hoff[q]);
     dfree(g, g->hep[q]);
   }
+  for (auto& b : g->ws) dfree(g, b);
+  dfree(g, g->spare_off);
+  dfree(g, g->spare_ep);
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   if (g->pin) cudaFreeHost(g->pin);
