@@ -173,20 +173,23 @@ def run_reference(a, rank, world):
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def algorithmic_bytes(kind, st, ncol, R_list, nfam):
+def algorithmic_bytes(kind, st, ncol, R_list, nfam, fused=False):
     """Unique HBM bytes the method must move, per kernel kind, summed over the op's
     launches of that kind: every array the kernel must read
     or write, counted once -- re-reads (the COUNT/WRITE recomputation, halo rows,
     the two output rows that read each level list, L1/L2 re-use) are not algorithmic.
       input CSR     8 B/column offset + 8 B/interval               (n_in)
       S_Mid pieces  8 B z-pair + 1 B kappa per piece, 4 B count per column   (n_mid)
-      level sets    8 B/interval (n_lev) + 1 B count per (column, direction, level)
-      output        8 B/interval (n_out) + 4 B count per column (staging), then CSR"""
+      level sets    8 B/interval (n_lev) + 2 B count per (column, level)
+      output        8 B/interval (n_out) + 4 B count per column (staging), then CSR
+    fused: the shell's two pass-1 families ran as one sweep (p1_dual_kernel), which reads
+    the input once."""
     n_in, m, nl, n_out = st["n_in"], st["n_mid"], st["n_lev"], st["n_out"]
     off = 8 * (ncol + 1)
     lev_cnt = sum(2 * (R + 1) * ncol for R in R_list)
     if kind == "pass1":          # read the input CSR, write pieces + counts
-        return nfam * (off + 8 * n_in + 4 * ncol) + 9 * m
+        reads = 1 if fused else nfam
+        return reads * (off + 8 * n_in) + nfam * 4 * ncol + 9 * m
     if kind == "levels":         # read pieces + counts, write level slots + counts
         return nfam * 4 * ncol + 9 * m + 8 * nl + lev_cnt
     if kind == "pass2":          # read level slots + counts, write staged output + counts
@@ -284,7 +287,11 @@ def run_b200(a, rank, world, local_rank):
     nfam = 2 if a.op == "shell" else 1
     R_list = [R] * nfam
     dom = max((k for k in dx.KERNEL_NAMES if k not in ("scan", "other")), key=lambda k: kern_ms[k])
-    byts = algorithmic_bytes(dom, st, ncol_local, R_list, nfam)
+    # the library fuses the shell's pass-1 families when r_out and r_in share R <= 16
+    # (DESIGN.md p1_dual_kernel; DEXEL_NO_FUSE=1 turns it off)
+    fused = (a.op == "shell" and R <= 16 and os.environ.get("DEXEL_NO_FUSE", "0") in ("", "0")
+             and os.environ.get("DEXEL_NO_PRUNE", "0") in ("", "0"))
+    byts = algorithmic_bytes(dom, st, ncol_local, R_list, nfam, fused)
     t_dom = kern_ms[dom] / a.steps / 1e3            # s per step for that kernel kind
     achieved = byts / t_dom / 1e9 if t_dom > 0 else 0.0
     traffic = None

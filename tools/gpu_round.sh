@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${tag}_launches.log 2>&1
 python tools/run_op.py C5 shell 16 1 > gpurun_out/${tag}_runop.log 2>&1 && \
 PROFILE_LAST=1 ncu --set full --clock-control none --profile-from-start off \
-  -k regex:"p1_kernel|levels_kernel|pass2s_kernel" -c 60 \
+  -k regex:"p1_kernel|p1_dual_kernel|levels_kernel|pass2s_kernel" -c 60 \
   -o /tmp/${tag}_full python tools/run_op.py C5 shell 16 3 > gpurun_out/${tag}_ncu.log 2>&1
 echo "done rc=$?" >> gpurun_out/${tag}_ncu.log
 # the report itself stays on the box (tens of MB): bring back its raw page and the summaries
