@@ -110,6 +110,20 @@ dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst
 dexel_status dexel_open(dexel_grid src, float r, dexel_grid dst);
 dexel_status dexel_close(dexel_grid src, float r, dexel_grid dst);
 
+/* 2D slice offsets (PAPER.md:422-487 the 2D uniform offset of a slice,
+ * :584 "the 2D dilations can be performed completely independently in every slice"): every
+ * grid row j is one 2D slice -- its columns along x, segments along z -- and is offset on its
+ * own, by a disk of radius r in the (x, z) plane:
+ *   dexel_dilate_slices:  dst row j := D_r(src row j)           (Eq. 1 restricted to the plane)
+ *   dexel_erode_slices:   dst row j := E_r(src row j) = U_j \ D_r(U_j \ src row j)
+ *   dexel_shell_slices:   dst row j := D_rout(row j) \ E_rin(row j)
+ * Each equals the 3D op on a grid with the single row j (reading R6 per slice).
+ * Computed as pass 1 along x and the level set L_0 alone (no pass along y, no halo: a y-slab
+ * handle needs no dexel_upload_halo).  Same argument rules as dexel_dilate. */
+dexel_status dexel_dilate_slices(dexel_grid src, float r, dexel_grid dst);
+dexel_status dexel_erode_slices(dexel_grid src, float r, dexel_grid dst);
+dexel_status dexel_shell_slices(dexel_grid src, float r_out, float r_in, dexel_grid dst);
+
 /* Attach halo rows (multi-GPU slabs): side 0 = the nrows global rows directly
  * below y0, side 1 = the nrows rows directly above y1 (row-major CSR of
  * nrows*nx columns, same conventions and validation as dexel_upload).  nrows

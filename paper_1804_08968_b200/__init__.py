@@ -24,7 +24,7 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_open", "dexel_close",
-           "dexel_size",
+           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows"]
@@ -78,6 +78,9 @@ def lib():
             "dexel_shell": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
             "dexel_open": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_close": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_dilate_slices": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_erode_slices": ([vp, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_shell_slices": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
             "dexel_size": ([vp, u64p], ctypes.c_int),
             "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
             "dexel_pass1": ([vp, ctypes.c_float, ctypes.c_int, vp, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
@@ -273,6 +276,24 @@ def dexel_erode(src: Grid, r: float, dst: Grid) -> Grid:
 
 def dexel_shell(src: Grid, r_out: float, r_in: float, dst: Grid) -> Grid:
     _check(lib().dexel_shell(src.h, float(r_out), float(r_in), dst.h))
+    return dst
+
+
+def dexel_dilate_slices(src: Grid, r: float, dst: Grid) -> Grid:
+    """Every row on its own as a 2D slice (x, z): dst row j := D_r(src row j) (SURVEY NEXT #2)."""
+    _check(lib().dexel_dilate_slices(src.h, float(r), dst.h))
+    return dst
+
+
+def dexel_erode_slices(src: Grid, r: float, dst: Grid) -> Grid:
+    """Every row on its own as a 2D slice: dst row j := E_r(src row j)."""
+    _check(lib().dexel_erode_slices(src.h, float(r), dst.h))
+    return dst
+
+
+def dexel_shell_slices(src: Grid, r_out: float, r_in: float, dst: Grid) -> Grid:
+    """Every row on its own as a 2D slice: dst row j := D_rout(row j) minus E_rin(row j)."""
+    _check(lib().dexel_shell_slices(src.h, float(r_out), float(r_in), dst.h))
     return dst
 
 

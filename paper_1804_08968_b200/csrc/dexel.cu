@@ -513,7 +513,9 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
 // (pre != nullptr: the family's pieces were computed already, by run_pass1_dual)
 dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, const float* prune,
                         int complement, int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev,
-                        const PieceSlots* pre = nullptr) {
+                        const PieceSlots* pre = nullptr, bool slices = false) {
+  // slices: only L_0 is needed (pass 2 reads dy = 0), so only the first chunk of levels runs
+  const int nlev_compute = slices ? 1 : R + 1;
   dexel_status s;
   PieceSlots P;
   if (pre) P = *pre;
@@ -523,6 +525,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   if ((s = T.get(64, (void**)&flags))) return s;
   unsigned long long* nlev = (unsigned long long*)(flags + 8);
   L->R = R;
+  L->ry = slices ? 0 : R;
   L->nx = src.nx;
   L->nrows = lrn;
   L->row0 = lr0;
@@ -538,8 +541,8 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17};
   int max_chunk = 17;   // measured on B200 (branch-free emission): 17 beats 12 at r = 16 and 32
   if (const char* e = std::getenv("DEXEL_LV_CHUNK")) max_chunk = std::max(2, std::min(17, std::atoi(e)));
-  const int nchunk = (R + 1 + max_chunk - 1) / max_chunk;
-  const int per = (R + 1 + nchunk - 1) / nchunk;
+  const int nchunk = (nlev_compute + max_chunk - 1) / max_chunk;
+  const int per = (nlev_compute + nchunk - 1) / nchunk;
   int lmax = 17;
   for (int v : kChunk)
     if (v >= per) { lmax = v; break; }
@@ -677,7 +680,7 @@ void set_empty(dexel_grid g) {
   g->n = 0;
 }
 
-dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
+dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst, bool slices) {
   const double op_t0 = now_s();
   g_t_alloc = g_t_sync = g_t_free = g_t_info = 0.0;
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
@@ -698,14 +701,15 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   }
   dexel_stats stats{};
   Temps T(src, &stats);
-  // halo rows (y-slabs): the op reads rows [y0 - hlo, y1 + hhi) and writes [y0, y1)
-  const int Rmax = Ra > Rb ? Ra : Rb;
+  // halo rows (y-slabs): the op reads rows [y0 - hlo, y1 + hhi) and writes [y0, y1).
+  // Slices (2D offsets of every row on its own) reach no other row: no halo, no band overlap.
+  const int Rmax = slices ? 0 : (Ra > Rb ? Ra : Rb);
   const int need_lo = src->d.y0 < Rmax ? src->d.y0 : Rmax;
   const int need_hi = src->d.ny - src->d.y1 < Rmax ? src->d.ny - src->d.y1 : Rmax;
   if (src->hrows[0] < need_lo || src->hrows[1] < need_hi)
     return fail(DEXEL_EINVAL, "slab halo too small: need " + std::to_string(need_lo) + " rows below and " +
                                   std::to_string(need_hi) + " above (dexel_upload_halo)");
-  const int hlo = src->hrows[0], hhi = src->hrows[1];
+  const int hlo = slices ? 0 : src->hrows[0], hhi = slices ? 0 : src->hrows[1];
   const int nrows_ext = hlo + src->nrows + hhi;
   const uint64_t* ext_off = (const uint64_t*)src->off.p;
   const float* ext_ep = (const float*)src->ep.p;
@@ -819,13 +823,13 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       }
       // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
       if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
-                          &stats.n_lev, fused ? &PA : nullptr))) {
+                          &stats.n_lev, fused ? &PA : nullptr, slices))) {
         set_empty(dst);
         return s;
       }
       if (op == OP_SHELL) {
         if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev,
-                            fused ? &PB : nullptr))) {
+                            fused ? &PB : nullptr, slices))) {
           set_empty(dst);
           return s;
         }
@@ -904,8 +908,8 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
 }
 
 // an op that ran out of device memory drops the cached band budget (the next op re-queries)
-dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst) {
-  const dexel_status s = run_op_impl(op, src, r_a, r_b, dst);
+dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst, bool slices = false) {
+  const dexel_status s = run_op_impl(op, src, r_a, r_b, dst, slices);
   if (s == DEXEL_ENOMEM && src) src->band_budget = 0;
   return s;
 }
@@ -1143,6 +1147,21 @@ dexel_status dexel_erode(dexel_grid src, float r, dexel_grid dst) {
 dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst) {
   g_err.clear();
   return run_op(OP_SHELL, src, r_out, r_in, dst);
+}
+
+dexel_status dexel_dilate_slices(dexel_grid src, float r, dexel_grid dst) {
+  g_err.clear();
+  return run_op(OP_DILATE, src, r, r, dst, true);
+}
+
+dexel_status dexel_erode_slices(dexel_grid src, float r, dexel_grid dst) {
+  g_err.clear();
+  return run_op(OP_ERODE, src, r, r, dst, true);
+}
+
+dexel_status dexel_shell_slices(dexel_grid src, float r_out, float r_in, dexel_grid dst) {
+  g_err.clear();
+  return run_op(OP_SHELL, src, r_out, r_in, dst, true);
 }
 
 }  // extern "C"

@@ -55,6 +55,7 @@ struct LevelSlots {
   uint16_t* cnt;     // [nrows][R+1][nx]  list lengths (<= 255); LV_IN_ARENA set: the list is in the arena
   float2* z;         // [nrows][cap+1][R+2][nx]  (unclipped; slot 0 dummy; level R+1 of the last slot = spill cell)
   int R, cap, nx, nrows;
+  int ry;            // row offsets pass 2 reads: |dy| <= ry (R; 0 for slices, 2D offsets of each row)
   int row0;          // row (in the op's extended-row numbering) of slot row 0
   // columns with a list longer than cap keep all their lists in the overflow arena:
   // list k of overflow slot q at ovf_z[(q*(R+1) + k)*(LV_OVF_CAP+1) + t], t = 1..255 (0 dummy)

@@ -125,8 +125,8 @@ template <int T>
 __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A,
                                           float2* scratch, int cap, unsigned* need) {
   A.n = 0;
-  const int dlo = max(-L.R, L.row0 - jg), dhi = min(L.R, L.row0 + L.nrows - 1 - jg);
-  const int nt = 2 * L.R + 1;
+  const int dlo = max(-L.ry, L.row0 - jg), dhi = min(L.ry, L.row0 + L.nrows - 1 - jg);
+  const int nt = 2 * L.ry + 1;
   auto dy_of = [](int t) { return (t & 1) ? ((t + 1) >> 1) : -(t >> 1); };
   auto count = [&](int t) -> int {
     if (t >= nt) return 0;

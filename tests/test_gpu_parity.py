@@ -473,3 +473,81 @@ def test_open_close_match_oracle_composition(dx, name_or_seed, r):
     check(off, ep, ref, what=f"clean r={r}")
     for g in (src, dst, dst2):
         g.close()
+
+
+# ---------------------------------------------------------------- 2D slice offsets (NEXT #2)
+def _row_grid(host, j):
+    """row j of a host grid as a grid of its own (ny = 1): the 2D slice (x, z)."""
+    nx = host.nx
+    o = np.asarray(host.off[j * nx:(j + 1) * nx + 1], dtype=np.uint64)
+    a, b = int(o[0]), int(o[-1])
+    return G.Grid(nx, 1, (o - np.uint64(a)).astype(np.uint64), np.asarray(host.ep[2 * a:2 * b], dtype=np.float32),
+                  host.z_lo, host.z_hi, host.z_ref, host.spacing)
+
+
+def _check_slices(dx, host, op, r, rows):
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    if op == "shell":
+        dx.dexel_shell_slices(src, r, r, dst)
+    else:
+        getattr(dx, "dexel_" + op + "_slices")(src, r, dst)
+    off, ep = dst.download()
+    for j in rows:
+        rg = _row_grid(host, int(j))
+        ref = O.shell(rg, r, r) if op == "shell" else getattr(O, op)(rg, r)
+        o, z = take_columns(off, ep, np.arange(host.nx) + int(j) * host.nx)
+        res = compare(o, z, ref.off, ref.z, 1e-4)
+        assert res["ok"], (op, r, int(j), res)
+    src.close()
+    dst.close()
+
+
+@pytest.mark.parametrize("cfg,op,r", [("C1", "dilate", 3.0), ("C1", "erode", 3.0), ("C1", "shell", 3.0),
+                                      ("C2", "dilate", 4.0), ("C2", "erode", 4.0), ("C2", "shell", 4.0),
+                                      ("C2", "dilate", 16.0), ("C3", "erode", 8.0)])
+def test_slices_match_oracle_per_row(dx, cfg, op, r):
+    """2D slice offsets: every row of the grid offset on its own equals
+    the oracle's op on the one-row grid of that row (Eq. 1 in the (x, z) plane)."""
+    host = G.config(cfg)
+    rows = np.arange(host.ny) if host.ny <= 64 else np.random.default_rng(5).choice(host.ny, 24, replace=False)
+    _check_slices(dx, host, op, r, rows)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_slices_random_small(dx, seed):
+    """Random grids, radii incl. 0 and non-integer, all three ops, every row."""
+    rs = np.random.default_rng(100 + seed)
+    nx, ny = int(rs.integers(1, 70)), int(rs.integers(1, 9))
+    cols = []
+    for _ in range(nx * ny):
+        k = int(rs.integers(0, 4))
+        pts = np.sort(rs.uniform(-20, 20, 2 * k)).astype(np.float32)
+        cols.append([(float(pts[2 * t]), float(pts[2 * t + 1])) for t in range(k) if pts[2 * t] < pts[2 * t + 1]
+                     and (t == 0 or pts[2 * t] > pts[2 * t - 1])])
+    host = G.from_columns(nx, ny, cols, -20.0, 20.0)
+    for op in ("dilate", "erode", "shell"):
+        for r in (0.0, 1.0, 2.5, 7.0):
+            _check_slices(dx, host, op, r, np.arange(ny))
+
+
+def test_slices_differ_from_3d_and_match_ny1(dx):
+    """On a one-row grid the slice op is the 3D op (bitwise); on a taller grid it is not
+    (rows do not reach each other), and the slab halo is not needed."""
+    host = G.config("C1")
+    r = 3.0
+    rg = _row_grid(host, 32)
+    a = dx.Grid.from_host(rg)
+    d3, d2 = dx.Grid.like(a), dx.Grid.like(a)
+    dx.dexel_dilate(a, r, d3)
+    dx.dexel_dilate_slices(a, r, d2)
+    o3, e3 = d3.download()
+    o2, e2 = d2.download()
+    assert np.array_equal(o3, o2) and np.array_equal(e3, e2)
+    full = dx.Grid.from_host(host)
+    f3, f2 = dx.Grid.like(full), dx.Grid.like(full)
+    dx.dexel_dilate(full, r, f3)
+    dx.dexel_dilate_slices(full, r, f2)
+    assert f2.size() < f3.size() or not np.array_equal(f2.download()[1], f3.download()[1])
+    for g in (a, d3, d2, full, f3, f2):
+        g.close()

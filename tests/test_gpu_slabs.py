@@ -26,7 +26,7 @@ def dx():
 def run_full(dx, host, op, r):
     src = dx.Grid.from_host(host)
     dst = dx.Grid.like(src)
-    getattr(dx, "dexel_" + op)(src, r, *( (r,) if op == "shell" else ()), dst)
+    getattr(dx, "dexel_" + op)(src, r, *( (r,) if op.startswith("shell") else ()), dst)
     return dst.download()
 
 
@@ -87,3 +87,29 @@ def test_slab_missing_halo_rejected(dx):
         dx.dexel_dilate(src, 3.0, dst)
     src.upload_halo(0, *csr_rows(host.off, host.ep, host.nx, y0 - 3, 3), 3)
     dx.dexel_dilate(src, 3.0, dst)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("op", ["dilate_slices", "erode_slices", "shell_slices"])
+def test_slice_ops_on_slabs_need_no_halo(dx, world, op):
+    """2D slice offsets read no other row: y-slab handles without any halo give, concatenated,
+    bitwise the single-handle result."""
+    host = G.config("C2")
+    r = 4.0
+    full = run_full(dx, host, op, r)
+    offs, eps = [], []
+    for g in range(world):
+        y0, y1 = slab_bounds(host.ny, world, g)
+        src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi, host.z_ref, 1.0, 0, None, y0, y1, g, world)
+        src.upload(*csr_rows(host.off, host.ep, host.nx, y0, y1 - y0))
+        dst = dx.Grid.like(src)
+        getattr(dx, "dexel_" + op)(src, r, *((r,) if op == "shell_slices" else ()), dst)
+        o, e = dst.download()
+        offs.append(o)
+        eps.append(e)
+    base, o_all = 0, [np.zeros(1, np.uint64)]
+    for o in offs:
+        o_all.append(o[1:] + np.uint64(base))
+        base += int(o[-1])
+    assert np.array_equal(np.concatenate(o_all), full[0])
+    assert np.array_equal(np.concatenate(eps), full[1])
