@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--op", default=None, choices=[None, "dilate", "erode", "shell"])
+    ap.add_argument("--op", default=None, choices=[None, "dilate", "erode", "shell", "dilate_slices", "erode_slices",
+                                                   "shell_slices"])
     ap.add_argument("--r", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -115,6 +116,20 @@ def oracle_band(host, op, r, rows, nthreads):
     import oracle as O
     j0 = host.ny // 2 - rows // 2
     cols = np.arange(j0 * host.nx, (j0 + rows) * host.nx, dtype=np.int64)
+    if op.endswith("_slices"):   # 2D slice offsets: the oracle op on each row's one-row grid
+        import dexelgen as G
+        base = op[:-len("_slices")]
+        t = time.perf_counter()
+        for j in range(j0, j0 + rows):
+            o = np.asarray(host.off[j * host.nx:(j + 1) * host.nx + 1], dtype=np.uint64)
+            a0, b0 = int(o[0]), int(o[-1])
+            rg = G.Grid(host.nx, 1, o - np.uint64(a0), np.asarray(host.ep[2 * a0:2 * b0], dtype=np.float32),
+                        host.z_lo, host.z_hi, host.z_ref, host.spacing)
+            if base == "shell":
+                O.shell(rg, r, r, nthreads=nthreads)
+            else:
+                getattr(O, base)(rg, r, nthreads=nthreads)
+        return len(cols), time.perf_counter() - t
     t = time.perf_counter()
     if op == "shell":
         O.shell(host, r, r, cols=cols, nthreads=nthreads)
@@ -131,6 +146,8 @@ def default_band_rows(cfg, op, r):
     n = {"C1": 64, "C2": 64, "C3": 16, "C4": 8, "C5": 16}[cfg]
     if cfg == "C4" and r >= 32:
         n = 2
+    if op and op.endswith("_slices"):   # 2D: about 2R+1 times less work per output column
+        n = min(n * 16, {"C1": 64, "C2": 512, "C3": 1024, "C4": 2048, "C5": 4096}[cfg])
     return n
 
 
@@ -229,7 +246,8 @@ def run_b200(a, rank, world, local_rank):
     def step():
         if world > 1:
             with torch.cuda.stream(stream):
-                slab.refresh_halos(R)          # NCCL send/recv of the R boundary rows (data-path exchange)
+                if not a.op.endswith("_slices"):   # (2D slice offsets read no other row)
+                    slab.refresh_halos(R)          # NCCL send/recv of the R boundary rows (data-path exchange)
         slab.op(a.op, a.r)
 
     def barrier():
@@ -284,12 +302,12 @@ def run_b200(a, rank, world, local_rank):
     # ---- roofline for the dominant kernel
     peak, peak_src = peaks()
     R = int(np.floor(a.r))
-    nfam = 2 if a.op == "shell" else 1
-    R_list = [R] * nfam
+    nfam = 2 if a.op.startswith("shell") else 1
+    R_list = [0 if a.op.endswith("_slices") else R] * nfam   # (slices: only L_0 is built and read)
     dom = max((k for k in dx.KERNEL_NAMES if k not in ("scan", "other")), key=lambda k: kern_ms[k])
     # the library fuses the shell's pass-1 families when r_out and r_in share R <= 16
     # (DESIGN.md p1_dual_kernel; DEXEL_NO_FUSE=1 turns it off)
-    fused = (a.op == "shell" and R <= 16 and os.environ.get("DEXEL_NO_FUSE", "0") in ("", "0")
+    fused = (a.op.startswith("shell") and R <= 16 and os.environ.get("DEXEL_NO_FUSE", "0") in ("", "0")
              and os.environ.get("DEXEL_NO_PRUNE", "0") in ("", "0"))
     byts = algorithmic_bytes(dom, st, ncol_local, R_list, nfam, fused)
     t_dom = kern_ms[dom] / a.steps / 1e3            # s per step for that kernel kind

@@ -130,10 +130,10 @@ class Slab:
 
     def op(self, op: str, r: float, r2: Optional[float] = None):
         dx = self.dx
-        if op == "dilate":
-            dx.dexel_dilate(self.src, r, self.dst)
-        elif op == "erode":
-            dx.dexel_erode(self.src, r, self.dst)
+        if op in ("dilate", "erode", "dilate_slices", "erode_slices"):
+            getattr(dx, "dexel_" + op)(self.src, r, self.dst)
+        elif op in ("shell", "shell_slices"):
+            getattr(dx, "dexel_" + op)(self.src, r, r if r2 is None else r2, self.dst)
         else:
-            dx.dexel_shell(self.src, r, r if r2 is None else r2, self.dst)
+            raise ValueError(f"unknown op {op!r}")
         return self.dst

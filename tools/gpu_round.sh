@@ -4,7 +4,8 @@ tag=${1:-r01}
 python bench.py --steps 5 --warmup 3 > gpurun_out/${tag}_bench_c5.json 2> gpurun_out/${tag}_bench_c5.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.json 2> gpurun_out/${tag}_bench_reference.err
 : > gpurun_out/${tag}_bench_c4c3.jsonl
-for a in "C4 dilate 1" "C4 dilate 4" "C4 dilate 16" "C4 dilate 64" "C3 dilate 8" "C2 shell 4"; do
+for a in "C4 dilate 1" "C4 dilate 4" "C4 dilate 16" "C4 dilate 64" "C3 dilate 8" "C2 shell 4" \
+         "C4 dilate_slices 16" "C5 shell_slices 16" "C3 erode_slices 8"; do
   set -- $a
   timeout 600 python bench.py --config $1 --op $2 --r $3 --steps 5 --warmup 3 --no-cpu >> gpurun_out/${tag}_bench_c4c3.jsonl 2>> gpurun_out/${tag}_bench_c4c3.err
 done
