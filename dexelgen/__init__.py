@@ -208,6 +208,34 @@ CONFIGS = {
 }
 
 
+def shape_config(name: str):
+    """The analytic solid of a shape config (C1, C2, C4, C5) as arrays, without rasterising:
+    (n, zmin, zmax, sph float64[k,4], sph_sign int32[k], box float64[m,6], box_sign int32[m])."""
+    k = int(name[1])
+    seed = SEED_BASE + k
+    N = CONFIGS[name]["n"]
+    box = np.zeros((0, 6))
+    if name == "C1":
+        sph, ssg = np.array([(32.0, 32.0, 32.0, 20.0)]), np.array([1])
+        box = np.array([(10.0, 25.0, 40.0, 55.0, 5.0, 50.0)])
+    elif name == "C2":
+        pos, _ = _random_spheres(seed, 200, 0, N, (5.0, 40.0), (0.0, 0.0))
+        kb = np.arange(50, dtype=np.uint64)
+        corner = rng_uniform(seed, 4, 3 * kb[:, None] + np.arange(3, dtype=np.uint64)[None, :]) * N
+        edge = 8.0 + 56.0 * rng_uniform(seed, 5, 3 * kb[:, None] + np.arange(3, dtype=np.uint64)[None, :])
+        hi = np.minimum(corner + edge, N)
+        box = np.stack([corner[:, 0], hi[:, 0], corner[:, 1], hi[:, 1], corner[:, 2], hi[:, 2]], axis=1)
+        sph, ssg = pos, np.ones(len(pos))
+    elif name in ("C4", "C5"):
+        npos, nneg, rr = (2000, 1000, (10.0, 120.0)) if name == "C4" else (20000, 10000, (8.0, 200.0))
+        pos, neg = _random_spheres(seed, npos, nneg, N, rr, rr)
+        sph, ssg = np.concatenate([pos, neg]), np.array([1] * len(pos) + [-1] * len(neg))
+    else:
+        raise KeyError(f"{name} is not a shape config")
+    return (N, 0.0, float(N), np.asarray(sph, np.float64).reshape(-1, 4), np.asarray(ssg, np.int32),
+            np.asarray(box, np.float64).reshape(-1, 6), np.ones(len(box), np.int32))
+
+
 def config(name: str, nthreads: int | None = None) -> Grid:
     """Build one of BASELINE.json's configs (C1..C5) deterministically."""
     k = int(name[1])

@@ -124,6 +124,26 @@ dexel_status dexel_dilate_slices(dexel_grid src, float r, dexel_grid dst);
 dexel_status dexel_erode_slices(dexel_grid src, float r, dexel_grid dst);
 dexel_status dexel_shell_slices(dexel_grid src, float r_out, float r_in, dexel_grid dst);
 
+/* GPU dexelisation of analytic solids (PAPER.md:114-118 dexel buffers,
+ * :42 / :170 CSG in dexel space): replace g's contents (its rows [y0, y1)) with the solid
+ *   (U spheres/boxes of sign +1) \ (U spheres/boxes of sign -1)
+ * rasterised onto the ray lattice (column (i,j) at ((i+1/2)s, (j+1/2)s), s = 1):
+ *   sph:      double[nsph][4]  (cx, cy, cz, R), world coordinates; sph_sign int32[nsph] (+1 / -1)
+ *   box:      double[nbox][6]  (x0, x1, y0, y1, z0, z1), z0 <= z1; a column is inside when its
+ *             centre is in [x0,x1] x [y0,y1]; box_sign int32[nbox]
+ *   zmin, zmax: the world z domain; the handle's frame must be z_ref = (zmin+zmax)/2,
+ *             z_lo = fl32(zmin - z_ref), z_hi = fl32(zmax - z_ref) (else DEXEL_EINVAL)
+ *   src_on_device: 0 host / 1 device arrays (read during the call).
+ * Per column in fp64 without contraction: sphere chords [cz -+ sqrt(R^2 - dy^2 - dx^2)], the
+ * unions of closed chords per sign, their difference, clipped to [zmin, zmax], shifted to the
+ * local frame, rounded to fp32 and canonicalised -- bitwise the host generator
+ * (dexelgen/dexelgen.c) that builds the configs.  A column needing more than 64 chord
+ * intervals per sign or 32 output intervals -> DEXEL_EOVERFLOW (grid unchanged).
+ * Synchronises the stream. */
+dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int nsph, const double* sph,
+                                    const int32_t* sph_sign, int nbox, const double* box,
+                                    const int32_t* box_sign, int src_on_device);
+
 /* Attach halo rows (multi-GPU slabs): side 0 = the nrows global rows directly
  * below y0, side 1 = the nrows rows directly above y1 (row-major CSR of
  * nrows*nx columns, same conventions and validation as dexel_upload).  nrows

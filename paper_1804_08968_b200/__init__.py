@@ -24,7 +24,7 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_open", "dexel_close",
-           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_size",
+           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows"]
@@ -81,6 +81,8 @@ def lib():
             "dexel_dilate_slices": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_erode_slices": ([vp, ctypes.c_float, vp], ctypes.c_int),
             "dexel_shell_slices": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
+            "dexel_rasterize_shapes": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, ctypes.c_int, vp,
+                                        vp, ctypes.c_int], ctypes.c_int),
             "dexel_size": ([vp, u64p], ctypes.c_int),
             "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
             "dexel_pass1": ([vp, ctypes.c_float, ctypes.c_int, vp, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
@@ -295,6 +297,19 @@ def dexel_shell_slices(src: Grid, r_out: float, r_in: float, dst: Grid) -> Grid:
     """Every row on its own as a 2D slice: dst row j := D_rout(row j) minus E_rin(row j)."""
     _check(lib().dexel_shell_slices(src.h, float(r_out), float(r_in), dst.h))
     return dst
+
+
+def dexel_rasterize_shapes(g: Grid, zmin: float, zmax: float, sph=None, sph_sign=None, box=None, box_sign=None) -> Grid:
+    """GPU dexelisation: g := (U solid spheres/boxes) minus (U void ones) on
+    g's rows.  sph: float64[n,4] (cx,cy,cz,R); box: float64[m,6] (x0,x1,y0,y1,z0,z1); signs +1/-1."""
+    sph = np.ascontiguousarray(np.zeros((0, 4)) if sph is None else sph, dtype=np.float64).reshape(-1, 4)
+    box = np.ascontiguousarray(np.zeros((0, 6)) if box is None else box, dtype=np.float64).reshape(-1, 6)
+    ss = np.ascontiguousarray(np.ones(len(sph)) if sph_sign is None else sph_sign, dtype=np.int32)
+    bs = np.ascontiguousarray(np.ones(len(box)) if box_sign is None else box_sign, dtype=np.int32)
+    _check(lib().dexel_rasterize_shapes(g.h, float(zmin), float(zmax), len(sph), sph.ctypes.data if len(sph) else None,
+                                        ss.ctypes.data if len(ss) else None, len(box),
+                                        box.ctypes.data if len(box) else None, bs.ctypes.data if len(bs) else None, 0))
+    return g
 
 
 def dexel_pass1(src: Grid, r: float, complement: bool = False):

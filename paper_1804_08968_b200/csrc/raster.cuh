@@ -1,0 +1,170 @@
+// raster.cuh -- GPU dexelisation of analytic solids: spheres and
+// axis-aligned boxes, each solid (+1) or void (-1), rasterised onto the ray lattice as the
+// canonical fp32 dexel CSR of (U solids) \ (U voids) (PAPER.md:114-118 dexel buffers,
+// :170 / :42 "CSG operations can be carried out easily in dexel space").
+//
+// Column (i, j) is the ray at ((i + 1/2) s, (j + 1/2) s), s = 1.  Per column, in fp64 with no
+// contraction (every product and sum rounded on its own, as the host generator computes it):
+//   sphere (cx, cy, cz, R): rr = R*R - dy*dy, dy = y - cy; if rr > 0 and the column lies in
+//     [ceil(cx - sqrt(rr) - 1/2), floor(cx + sqrt(rr) - 1/2)] and q = rr - dx*dx > 0,
+//     dx = x - cx, the chord is [cz - sqrt(q), cz + sqrt(q)];
+//   box (x0, x1, y0, y1, z0, z1): y in [y0, y1] and the column in [ceil(x0 - 1/2), floor(x1 - 1/2)]
+//     give the chord [z0, z1].
+// The column's solid is union(solid chords) \ union(void chords) (closed intervals, touching
+// merges), clipped to [zmin, zmax], shifted to the local frame z - zref, rounded to fp32 and
+// canonicalised (touching after rounding merges, zero length after rounding drops).  The
+// result equals dexelgen.c (the input generator) bit for bit: the unions of closed intervals
+// are unique, so building them by insertion instead of sort + sweep changes nothing, and every
+// endpoint is the same fp64 expression rounded once to fp32.
+//
+// One thread per column; a block is a tile of RT_X x RT_Y columns (a warp = 32 consecutive
+// columns of a row) and walks the tile's shape list (host-binned, conservative); every lane
+// reads the same shape (broadcast load).  The unions live in per-thread local memory.
+// Results go to a [t][column] staging array, then the scan and compact_kernel (pass2.cuh).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dexel {
+
+constexpr int RT_X = 32, RT_Y = 8;
+constexpr int RS_CAP = 64;     // intervals per union (solid chords, void chords) of one column
+constexpr int RS_OUT = 32;     // output intervals per column (staging)
+
+struct RasterArgs {
+  int nx, nrows, y0;           // local rows [0, nrows) are global rows y0 + jl
+  double zmin, zmax, zref;
+  int nsph;
+  const double* sph;           // [nsph][4] cx, cy, cz, R (world)
+  const int32_t* sph_sign;
+  int nbox;
+  const double* box;           // [nbox][6] x0, x1, y0, y1, z0, z1
+  const int32_t* box_sign;
+  const int64_t* tile_off;     // [ntiles + 1]
+  const int32_t* tile_ids;     // shape ids: sphere k -> k, box k -> nsph + k
+  int ntx;                     // tiles per tile row
+  float2* stage;               // [RS_OUT][ncol]
+  uint32_t* cnt;               // [ncol]
+  unsigned* flags;             // [0] a union or the output outgrew its capacity
+};
+
+// insert the closed interval [lo, hi] into the sorted disjoint union V[0..n) (touching merges)
+__device__ __forceinline__ void rs_union_insert(double2* V, int& n, double lo, double hi, bool& ovf) {
+  int p = 0;
+  while (p < n && V[p].y < lo) ++p;
+  if (p < n && V[p].x <= hi) {   // overlaps or touches V[p]: merge the run p..q
+    double nlo = fmin(lo, V[p].x), nhi = fmax(hi, V[p].y);
+    int q = p;
+    while (q + 1 < n && V[q + 1].x <= nhi) {
+      ++q;
+      nhi = fmax(nhi, V[q].y);
+    }
+    V[p] = make_double2(nlo, nhi);
+    const int drop = q - p;
+    if (drop) {
+      for (int t = q + 1; t < n; ++t) V[t - drop] = V[t];
+      n -= drop;
+    }
+    return;
+  }
+  if (n >= RS_CAP) {
+    ovf = true;
+    return;
+  }
+  for (int t = n; t > p; --t) V[t] = V[t - 1];
+  V[p] = make_double2(lo, hi);
+  ++n;
+}
+
+__global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
+  const int tile = blockIdx.x;
+  const int tx = tile % A.ntx, ty = tile / A.ntx;
+  const int i = tx * RT_X + threadIdx.x, jl = ty * RT_Y + threadIdx.y;
+  const bool live = i < A.nx && jl < A.nrows;
+  const double x = (double)i + 0.5, y = (double)(A.y0 + jl) + 0.5;
+  double2 P[RS_CAP], N[RS_CAP];
+  int np = 0, nn = 0;
+  bool ovf = false;
+  for (int64_t t = A.tile_off[tile]; t < A.tile_off[tile + 1]; ++t) {
+    const int id = A.tile_ids[t];
+    double lo, hi;
+    int sg;
+    if (id < A.nsph) {
+      const double* s = A.sph + 4 * (size_t)id;
+      const double dy = __dsub_rn(y, s[1]), R = s[3];
+      const double rr = __dsub_rn(__dmul_rn(R, R), __dmul_rn(dy, dy));
+      if (!(rr > 0.0)) continue;
+      const double hx = sqrt(rr);
+      const int i0 = (int)ceil(__dsub_rn(__dsub_rn(s[0], hx), 0.5));
+      const int i1 = (int)floor(__dsub_rn(__dadd_rn(s[0], hx), 0.5));
+      if (i < i0 || i > i1) continue;
+      const double dx = __dsub_rn(x, s[0]);
+      const double q = __dsub_rn(rr, __dmul_rn(dx, dx));
+      if (!(q > 0.0)) continue;
+      const double h = sqrt(q);
+      lo = __dsub_rn(s[2], h);
+      hi = __dadd_rn(s[2], h);
+      sg = A.sph_sign[id];
+    } else {
+      const int b = id - A.nsph;
+      const double* s = A.box + 6 * (size_t)b;
+      if (y < s[2] || y > s[3]) continue;
+      const int i0 = (int)ceil(__dsub_rn(s[0], 0.5)), i1 = (int)floor(__dsub_rn(s[1], 0.5));
+      if (i < i0 || i > i1) continue;
+      lo = s[4];
+      hi = s[5];
+      sg = A.box_sign[b];
+    }
+    if (!live) continue;
+    // (the host generator keeps chords with lo > hi out of nothing: none exist, h >= 0 and
+    // boxes have z0 <= z1 by construction; a degenerate box still enters its union as given)
+    if (sg > 0) rs_union_insert(P, np, lo, hi, ovf);
+    else rs_union_insert(N, nn, lo, hi, ovf);
+  }
+  if (!live) return;
+  const int64_t c = (int64_t)jl * A.nx + i;
+  const int64_t ncol = (int64_t)A.nrows * A.nx;
+  // difference P \ N (sorted, disjoint), then clip, shift, round, canonicalise
+  uint32_t k = 0;
+  float la = 0.f, lb = 0.f;    // last written output interval (merge target)
+  auto emit = [&](double dlo, double dhi) {
+    const double clo = dlo < A.zmin ? A.zmin : dlo;
+    const double chi = dhi > A.zmax ? A.zmax : dhi;
+    if (!(clo < chi)) return;
+    const float a = (float)__dsub_rn(clo, A.zref), b = (float)__dsub_rn(chi, A.zref);
+    if (k > 0 && a <= lb) {                 // touches / overlaps after rounding
+      if (b > lb) {
+        lb = b;
+        A.stage[(int64_t)(k - 1) * ncol + c] = make_float2(la, lb);
+      }
+      return;
+    }
+    if (!(a < b)) return;                   // zero length after rounding
+    if (k >= (uint32_t)RS_OUT) {
+      ovf = true;
+      return;
+    }
+    la = a;
+    lb = b;
+    A.stage[(int64_t)k * ncol + c] = make_float2(a, b);
+    ++k;
+  };
+  int jb = 0;
+  for (int ia = 0; ia < np; ++ia) {
+    double lo = P[ia].x;
+    const double hi = P[ia].y;
+    while (jb < nn && N[jb].y <= lo) ++jb;
+    int t = jb;
+    while (t < nn && N[t].x < hi) {
+      if (N[t].x > lo) emit(lo, N[t].x);
+      if (N[t].y > lo) lo = N[t].y;
+      if (lo >= hi) break;
+      ++t;
+    }
+    if (lo < hi) emit(lo, hi);
+  }
+  A.cnt[c] = k;
+  if (ovf) atomicOr(A.flags, 1u);
+}
+
+}  // namespace dexel

@@ -551,3 +551,77 @@ def test_slices_differ_from_3d_and_match_ny1(dx):
     assert f2.size() < f3.size() or not np.array_equal(f2.download()[1], f3.download()[1])
     for g in (a, d3, d2, full, f3, f2):
         g.close()
+
+
+# ---------------------------------------------------------------- GPU dexelisation (NEXT #3)
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
+def test_rasterize_shapes_bitwise_host_generator(dx, cfg):
+    """dexel_rasterize_shapes on the GPU gives bitwise the CSR the host generator
+    (dexelgen.c, fp64 per-column CSG) builds for the config."""
+    n, zmin, zmax, sph, ss, box, bs = G.shape_config(cfg)
+    host = G.config(cfg)
+    g = dx.Grid.from_host(host)          # (frame and a previous content to replace)
+    g2 = dx.Grid.like(g)
+    dx.dexel_rasterize_shapes(g2, zmin, zmax, sph, ss, box, bs)
+    off, ep = g2.download()
+    assert np.array_equal(off.astype(np.uint64), host.off.astype(np.uint64))
+    assert np.array_equal(ep, host.ep)
+    g.close()
+    g2.close()
+
+
+def test_rasterize_shapes_c5_slab(dx):
+    """C5 (20000 spheres minus 10000 voids) on a y-slab handle: its rows equal the host's."""
+    n, zmin, zmax, sph, ss, box, bs = G.shape_config("C5")
+    host = G.config("C5")
+    y0, y1 = 1500, 1628
+    g = dx.Grid(n, n, host.z_lo, host.z_hi, host.z_ref, 1.0, 0, None, y0, y1, 1, 3)
+    dx.dexel_rasterize_shapes(g, zmin, zmax, sph, ss, box, bs)
+    off, ep = g.download()
+    a, b = int(host.off[y0 * n]), int(host.off[y1 * n])
+    assert np.array_equal(off.astype(np.int64), host.off[y0 * n:y1 * n + 1].astype(np.int64) - a)
+    assert np.array_equal(ep, host.ep[2 * a:2 * b])
+    g.close()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_rasterize_shapes_random(dx, seed):
+    """Random spheres and boxes of both signs, partly outside the grid and the z domain, with
+    integer / half-integer placements (ties on column centres and touching chords)."""
+    rs = np.random.default_rng(200 + seed)
+    nx, ny = int(rs.integers(1, 90)), int(rs.integers(1, 40))
+    zmin, zmax = -5.0, float(rs.integers(10, 60))
+    k, m = int(rs.integers(0, 40)), int(rs.integers(0, 12))
+    sph = np.stack([rs.uniform(-10, nx + 10, k), rs.uniform(-10, ny + 10, k), rs.uniform(zmin - 5, zmax + 5, k),
+                    rs.uniform(0.3, 15, k)], axis=1)
+    if seed % 2:
+        sph[:, :3] = np.round(sph[:, :3] * 2) / 2
+        sph[:, 3] = np.round(sph[:, 3] * 2) / 2 + 0.5
+    x0, y0 = rs.uniform(-5, nx, m), rs.uniform(-5, ny, m)
+    z0 = rs.uniform(zmin - 3, zmax, m)
+    box = np.stack([x0, x0 + rs.uniform(0, 20, m), y0, y0 + rs.uniform(0, 20, m), z0, z0 + rs.uniform(0, 20, m)], axis=1)
+    if seed % 2:
+        box = np.round(box * 2) / 2
+    ss = np.where(rs.random(k) < 0.3, -1, 1).astype(np.int32)
+    bs = np.where(rs.random(m) < 0.3, -1, 1).astype(np.int32)
+    host = G.shapes(nx, ny, zmin, zmax, spheres=sph[ss > 0], voids=sph[ss < 0], boxes=box[bs > 0],
+                    box_voids=box[bs < 0])
+    g = dx.Grid(nx, ny, host.z_lo, host.z_hi, host.z_ref)
+    dx.dexel_rasterize_shapes(g, zmin, zmax, sph, ss, box, bs)
+    off, ep = g.download()
+    assert np.array_equal(off.astype(np.uint64), host.off.astype(np.uint64))
+    assert np.array_equal(ep, host.ep)
+    g.close()
+
+
+def test_rasterize_shapes_errors(dx):
+    host = G.config("C1")
+    g = dx.Grid.from_host(host)
+    before = g.download()
+    with pytest.raises(Exception):   # frame mismatch
+        dx.dexel_rasterize_shapes(g, 0.0, 32.0, np.array([(32.0, 32.0, 16.0, 4.0)]), np.array([1]))
+    after = g.download()
+    assert np.array_equal(before[1], after[1])
+    dx.dexel_rasterize_shapes(g, 0.0, 64.0)   # no shapes: the empty solid
+    assert g.size() == 0
+    g.close()
