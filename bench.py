@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--op", default=None, choices=[None, "dilate", "erode", "shell", "dilate_slices", "erode_slices",
-                                                   "shell_slices"])
+                                                   "shell_slices", "rasterize"])
     ap.add_argument("--r", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -168,6 +168,27 @@ def run_reference(a, rank, world):
     import dexelgen as G
     host = G.config(a.config)
     cores = host_cores()
+    if a.op == "rasterize":   # the host generator dexelgen.c on the whole grid
+        _, zmin_w, zmax_w, sph, ssg, box, bsg = G.shape_config(a.config)
+        ts = []
+        for it in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            G.shapes(host.nx, host.ny, zmin_w, zmax_w, spheres=sph[ssg > 0], voids=sph[ssg < 0],
+                     boxes=box[bsg > 0], box_voids=box[bsg < 0], nthreads=cores)
+            if it >= a.warmup:
+                ts.append(time.perf_counter() - t0)
+        tot = sum(ts)
+        v = host.ncol * len(ts) / tot
+        print(json.dumps({"impl": "reference", "metric": metric_name(a.op), "value": v, "unit": "columns/s",
+                          "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * tot / len(ts),
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic (seeded generator, DESIGN.md input recipe)",
+                          "config": {"workload": f"{a.config} rasterize", "grid": f"{host.nx}x{host.ny}"},
+                          "cpu_baseline": {"kind": "oracle", "cores": cores, "value": v,
+                                           "sample": "host generator dexelgen.c on the whole grid per step"},
+                          "e2e": {"value": v, "unit": "columns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
     rows = a.cpu_rows or max(1, default_band_rows(a.config, a.op, a.r) // 4)
     for _ in range(a.warmup):
         oracle_band(host, a.op, a.r, rows, cores)
@@ -211,6 +232,8 @@ def algorithmic_bytes(kind, st, ncol, R_list, nfam, fused=False):
         return nfam * 4 * ncol + 9 * m + 8 * nl + lev_cnt
     if kind == "pass2":          # read level slots + counts, write staged output + counts
         return 8 * nl + lev_cnt + 8 * n_out + 4 * ncol
+    if kind == "raster":         # (dexelisation) write the staged output + counts; shapes are KB
+        return 8 * n_out + 4 * ncol
     if kind == "compact":        # read staged output + counts + offsets, write the output CSR
         return 8 * n_out + 4 * ncol + off + 8 * n_out
     return 0
@@ -242,8 +265,16 @@ def run_b200(a, rank, world, local_rank):
     slab = Slab(host, rank, world, dev, stream.cuda_stream)
     src, dst = slab.src, slab.dst
     ncol_local = src.ncol   # columns this rank writes
+    # rasterize: a step dexelises the config's analytic solid into the grid
+    raster = a.op == "rasterize"
+    if raster:
+        _, zmin_w, zmax_w, sph, ssg, box, bsg = G.shape_config(a.config)
+    out_grid = src if raster else dst
 
     def step():
+        if raster:
+            dx.dexel_rasterize_shapes(src, zmin_w, zmax_w, sph, ssg, box, bsg)
+            return
         if world > 1:
             with torch.cuda.stream(stream):
                 if not a.op.endswith("_slices"):   # (2D slice offsets read no other row)
@@ -272,7 +303,7 @@ def run_b200(a, rank, world, local_rank):
     e0.record(stream)
     for _ in range(a.steps):
         step()
-        launches += dst.stats()["launches"]
+        launches += out_grid.stats()["launches"]
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -285,7 +316,7 @@ def run_b200(a, rank, world, local_rank):
     barrier()
     for _ in range(a.steps):
         step()
-        st = dst.stats()
+        st = out_grid.stats()
         for k in dx.KERNEL_NAMES:
             kern_ms[k] += st["kernel_ms"][k]
             kern_calls[k] += st["kernel_calls"][k]
@@ -296,13 +327,13 @@ def run_b200(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / a.steps
-    st = dst.stats()
+    st = out_grid.stats()
     value = ncol / (ms / 1e3)                 # whole-grid output columns / s (all ranks)
 
     # ---- roofline for the dominant kernel
     peak, peak_src = peaks()
     R = int(np.floor(a.r))
-    nfam = 2 if a.op.startswith("shell") else 1
+    nfam = 2 if a.op.startswith("shell") else (0 if a.op == "rasterize" else 1)
     R_list = [0 if a.op.endswith("_slices") else R] * nfam   # (slices: only L_0 is built and read)
     dom = max((k for k in dx.KERNEL_NAMES if k not in ("scan", "other")), key=lambda k: kern_ms[k])
     # the library fuses the shell's pass-1 families when r_out and r_in share R <= 16
@@ -329,7 +360,26 @@ def run_b200(a, rank, world, local_rank):
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
-    if not a.no_e2e and world == 1:
+    if not a.no_e2e and world == 1 and raster:
+        # the shapes from host arrays (copied inside the call) and the result CSR to pinned host memory
+        nout_cap = int(st["n_out"] * 1.1) + 1024
+        o_off = torch.empty(ncol + 1, dtype=torch.int64).pin_memory()
+        o_ep = torch.empty(2 * nout_cap, dtype=torch.float32).pin_memory()
+        L = dx.lib()
+        ke = max(1, min(a.steps, 5))
+        step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            step()
+            nout = src.size()
+            dx._check(L.dexel_download(src.h, o_off.data_ptr(), o_ep.data_ptr(), nout_cap, 0))
+        torch.cuda.synchronize()
+        e_ms = 1e3 * (time.perf_counter() - t0) / ke
+        e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
+               "h2d_bytes_per_step": int(sph.nbytes + ssg.nbytes + box.nbytes + bsg.nbytes),
+               "d2h_bytes_per_step": 8 * (ncol + 1) + 8 * nout, "ms_per_step": e_ms}
+    elif not a.no_e2e and world == 1:
         h_off = torch.from_numpy(host.off.view(np.int64)).pin_memory()
         h_ep = torch.from_numpy(host.ep).pin_memory()
         nout_cap = int(st["n_out"] * 1.1) + 1024
@@ -364,7 +414,16 @@ def run_b200(a, rank, world, local_rank):
 
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None
-    if not a.no_cpu and rank == 0 and world == 1:
+    if not a.no_cpu and rank == 0 and world == 1 and raster:
+        cores = host_cores()
+        t0 = time.perf_counter()
+        G.shapes(host.nx, host.ny, zmin_w, zmax_w, spheres=sph[ssg > 0], voids=sph[ssg < 0], boxes=box[bsg > 0],
+                 box_voids=box[bsg < 0], nthreads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": ncol / dt, "unit": "columns/s", "cores": cores, "kind": "oracle",
+               "sample": f"the host generator dexelgen.c (fp64 per-column CSG, the definition the GPU path is "
+                         f"tested bitwise against) on the whole {a.config} grid, {dt:.1f} s"}
+    elif not a.no_cpu and rank == 0 and world == 1:
         cores = host_cores()
         rows = a.cpu_rows or default_band_rows(a.config, a.op, a.r)
         ncols_s, dt = oracle_band(host, a.op, a.r, rows, cores)

@@ -200,7 +200,7 @@ dexel_status dexel_set_allocator(dexel_alloc_fn alloc, dexel_free_fn free_, void
  * (dexel_set_timing(1)), the summed device time and launch count of each
  * kernel kind, measured with CUDA events on the handle's stream:
  *   0 pass1, 1 pass1 overflow (list) launches, 2 levels, 3 pass2,
- *   4 compaction, 5 scan, 6 other, 7 reserved. */
+ *   4 compaction, 5 scan, 6 other, 7 rasterisation (dexel_rasterize_shapes). */
 #define DEXEL_NKERNELS 8
 typedef struct {
   uint64_t n_in, n_mid, n_lev, n_out;

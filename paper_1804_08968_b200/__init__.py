@@ -45,7 +45,7 @@ class dexel_desc(ctypes.Structure):
 
 
 NKERNELS = 8
-KERNEL_NAMES = ["pass1", "pass1_list", "levels", "pass2", "compact", "scan", "other", "reserved"]
+KERNEL_NAMES = ["pass1", "pass1_list", "levels", "pass2", "compact", "scan", "other", "raster"]
 
 
 class dexel_stats(ctypes.Structure):

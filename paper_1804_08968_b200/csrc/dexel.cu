@@ -155,7 +155,7 @@ void dfree(dexel_grid g, Buf& b) {
 }
 
 // per-op kernel accounting: launch counts always, CUDA-event device times when g_timing
-enum { K_P1 = 0, K_P1LIST = 1, K_LEV = 2, K_P2 = 3, K_COMPACT = 4, K_SCAN = 5, K_OTHER = 6 };
+enum { K_P1 = 0, K_P1LIST = 1, K_LEV = 2, K_P2 = 3, K_COMPACT = 4, K_SCAN = 5, K_OTHER = 6, K_RASTER = 7 };
 struct Prof {
   cudaStream_t st = nullptr;
   dexel_stats* s = nullptr;
@@ -1294,7 +1294,8 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
         for (int t = rg[id].t0; t <= rg[id].t1; ++t) tids[fill[(int64_t)u * ntx + t]++] = id;
   }
   dexel_status s;
-  Temps T(g);
+  dexel_stats stats{};
+  Temps T(g, &stats);
   double *dsph = nullptr, *dbox = nullptr;
   int32_t *dss = nullptr, *dbs = nullptr, *dtid = nullptr;
   int64_t* dtoff = nullptr;
@@ -1324,7 +1325,7 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   CK(cudaMemsetAsync(flags, 0, 64, g->stream));
   RasterArgs A{nx, nrows, y0, zmin, zmax, zref, nsph, dsph, dss, nbox, dbox, dbs, dtoff, dtid, ntx,
                stage, cnt, flags};
-  if (ntiles > 0) raster_kernel<<<(unsigned)ntiles, dim3(RT_X, RT_Y), 0, g->stream>>>(A);
+  if (ntiles > 0) LAUNCH(T, K_RASTER, raster_kernel<<<(unsigned)ntiles, dim3(RT_X, RT_Y), 0, g->stream>>>(A));
   CK(cudaGetLastError());
   unsigned hf = 0;
   {
@@ -1347,15 +1348,18 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
     return s;
   }
   if (ncol > 0)
-    compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, g->stream>>>(stage, cnt, (const uint64_t*)off.p, ncol,
-                                                                           (float2*)ep.p);
+    LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, g->stream>>>(
+                             stage, cnt, (const uint64_t*)off.p, ncol, (float2*)ep.p));
   CK(cudaGetLastError());
+  T.prof.finish();
   CK(timed_sync(g->stream));
   dfree(g, g->off);
   dfree(g, g->ep);
   g->off = off;
   g->ep = ep;
   g->n = n;
+  stats.n_out = n;
+  g->stats = stats;
   return DEXEL_OK;
 }
 
