@@ -1242,7 +1242,7 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
     return fail(DEXEL_EINVAL, "[zmin, zmax] must give the grid's frame: z_ref = (zmin + zmax)/2, "
                               "z_lo = fl32(zmin - z_ref), z_hi = fl32(zmax - z_ref)");
   CK(cudaSetDevice(g->d.device));
-  // the shapes on the host (binning) and on the device (the kernel)
+  // the shapes on the host (validation), then on the device (binning, the kernel)
   std::vector<double> hs((size_t)4 * nsph), hb((size_t)6 * nbox);
   std::vector<int32_t> hss(nsph), hbs(nbox);
   const cudaMemcpyKind k = src_on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
@@ -1256,49 +1256,17 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   }
   for (double v : hs) if (!std::isfinite(v)) return fail(DEXEL_EINVAL, "non-finite sphere parameter");
   for (double v : hb) if (!std::isfinite(v)) return fail(DEXEL_EINVAL, "non-finite box parameter");
-  // conservative tile binning (the kernel's per-column tests are exact)
   const int nx = g->d.nx, nrows = g->nrows, y0 = g->d.y0;
   const int ntx = (nx + RT_X - 1) / RT_X, nty = (nrows + RT_Y - 1) / RT_Y;
   const int64_t ntiles = (int64_t)ntx * nty;
-  std::vector<int64_t> toff(ntiles + 1, 0);
-  struct Rng { int t0, t1, u0, u1; };
-  std::vector<Rng> rg(nsph + nbox);
-  for (int id = 0; id < nsph + nbox; ++id) {
-    double xa, xb, ya, yb;
-    if (id < nsph) {
-      const double* q = &hs[4 * (size_t)id];
-      xa = q[0] - q[3]; xb = q[0] + q[3]; ya = q[1] - q[3]; yb = q[1] + q[3];
-    } else {
-      const double* q = &hb[6 * (size_t)(id - nsph)];
-      xa = q[0]; xb = q[1]; ya = q[2]; yb = q[3];
-    }
-    const double ia = std::floor(xa - 0.5) - 1, ib = std::ceil(xb - 0.5) + 1;
-    const double ja = std::floor(ya - 0.5) - 1 - y0, jb = std::ceil(yb - 0.5) + 1 - y0;
-    Rng r{1, 0, 1, 0};
-    if (ib >= 0 && ia <= nx - 1 && jb >= 0 && ja <= nrows - 1) {
-      r.t0 = (int)std::max(0.0, ia) / RT_X;
-      r.t1 = (int)std::min((double)nx - 1, ib) / RT_X;
-      r.u0 = (int)std::max(0.0, ja) / RT_Y;
-      r.u1 = (int)std::min((double)nrows - 1, jb) / RT_Y;
-    }
-    rg[id] = r;
-    for (int u = r.u0; u <= r.u1; ++u)
-      for (int t = r.t0; t <= r.t1; ++t) toff[(int64_t)u * ntx + t + 1]++;
-  }
-  for (int64_t t = 0; t < ntiles; ++t) toff[t + 1] += toff[t];
-  std::vector<int32_t> tids(std::max<int64_t>(1, toff[ntiles]));
-  {
-    std::vector<int64_t> fill(toff.begin(), toff.end() - 1);
-    for (int id = 0; id < nsph + nbox; ++id)
-      for (int u = rg[id].u0; u <= rg[id].u1; ++u)
-        for (int t = rg[id].t0; t <= rg[id].t1; ++t) tids[fill[(int64_t)u * ntx + t]++] = id;
-  }
+  const int nshape = nsph + nbox;
   dexel_status s;
   dexel_stats stats{};
   Temps T(g, &stats);
   double *dsph = nullptr, *dbox = nullptr;
   int32_t *dss = nullptr, *dbs = nullptr, *dtid = nullptr;
-  int64_t* dtoff = nullptr;
+  uint64_t* dtoff = nullptr;
+  uint32_t *tcnt = nullptr, *tcur = nullptr;
   const int64_t ncol = g->ncol;
   float2* stage = nullptr;
   uint32_t* cnt = nullptr;
@@ -1307,8 +1275,9 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   if ((s = T.get(sizeof(double) * hb.size() + 16, (void**)&dbox))) return s;
   if ((s = T.get(sizeof(int32_t) * hss.size() + 16, (void**)&dss))) return s;
   if ((s = T.get(sizeof(int32_t) * hbs.size() + 16, (void**)&dbs))) return s;
-  if ((s = T.get(sizeof(int64_t) * toff.size(), (void**)&dtoff))) return s;
-  if ((s = T.get(sizeof(int32_t) * tids.size(), (void**)&dtid))) return s;
+  if ((s = T.get(sizeof(uint64_t) * (ntiles + 1), (void**)&dtoff))) return s;
+  if ((s = T.get(sizeof(uint32_t) * (ntiles + 1) * 2, (void**)&tcnt))) return s;
+  tcur = tcnt + ntiles + 1;
   if ((s = T.get(sizeof(float2) * (size_t)RS_OUT * ncol + 16, (void**)&stage))) return s;
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&cnt))) return s;
   if ((s = T.get(64, (void**)&flags))) return s;
@@ -1320,8 +1289,16 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
     CK(cudaMemcpyAsync(dbox, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, g->stream));
     CK(cudaMemcpyAsync(dbs, hbs.data(), sizeof(int32_t) * hbs.size(), cudaMemcpyHostToDevice, g->stream));
   }
-  CK(cudaMemcpyAsync(dtoff, toff.data(), sizeof(int64_t) * toff.size(), cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(dtid, tids.data(), sizeof(int32_t) * tids.size(), cudaMemcpyHostToDevice, g->stream));
+  // tile binning on the device: count, scan, fill (conservative; the kernel's tests are exact)
+  const RasterBin Bn{nx, nrows, y0, ntx, nsph, nshape, dsph, dbox};
+  CK(cudaMemsetAsync(tcnt, 0, sizeof(uint32_t) * (ntiles + 1) * 2, g->stream));
+  const unsigned sb = (unsigned)((nshape + 255) / 256);
+  if (nshape) LAUNCH(T, K_RASTER, raster_bin_count<<<sb, 256, 0, g->stream>>>(Bn, tcnt));
+  uint64_t nids = 0;
+  if ((s = scan_counts(g, T, tcnt, (uint64_t)ntiles, dtoff, &nids))) return s;
+  if ((s = T.get(sizeof(int32_t) * (nids + 1), (void**)&dtid))) return s;
+  if (nshape) LAUNCH(T, K_RASTER, raster_bin_fill<<<sb, 256, 0, g->stream>>>(Bn, dtoff, tcur, dtid));
+  CK(cudaGetLastError());
   CK(cudaMemsetAsync(flags, 0, 64, g->stream));
   RasterArgs A{nx, nrows, y0, zmin, zmax, zref, nsph, dsph, dss, nbox, dbox, dbs, dtoff, dtid, ntx,
                stage, cnt, flags};
@@ -1335,28 +1312,31 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
     rb.get(0, &hf, sizeof(hf));
   }
   if (hf) return fail(DEXEL_EOVERFLOW, "a column needs more than 64 chord intervals per sign or 32 output intervals");
-  // offsets, then the endpoints (the grid is replaced only now)
-  Buf off, ep;
-  if ((s = dalloc(g, off, sizeof(uint64_t) * (ncol + 1)))) return s;
+  // offsets, then the endpoints: the grid is replaced only now, into its own buffers when they
+  // fit (a fresh allocation per call churns the stream-ordered pool); an error from here on
+  // leaves the grid empty
+  if (!g->off.p && (s = dalloc(g, g->off, sizeof(uint64_t) * (ncol + 1)))) return s;
   uint64_t n = 0;
-  if ((s = scan_counts(g, T, cnt, (uint64_t)ncol, (uint64_t*)off.p, &n))) {
-    dfree(g, off);
+  if ((s = scan_counts(g, T, cnt, (uint64_t)ncol, (uint64_t*)g->off.p, &n))) {
+    set_empty(g);
     return s;
   }
-  if ((s = dalloc(g, ep, sizeof(float2) * (n + 1)))) {
-    dfree(g, off);
-    return s;
+  {
+    const size_t need = sizeof(float2) * (n + 1);
+    if (!(g->ep.p && g->ep.bytes >= need && g->ep.bytes - need <= need / 4)) {
+      dfree(g, g->ep);
+      if ((s = dalloc(g, g->ep, need))) {
+        set_empty(g);
+        return s;
+      }
+    }
   }
   if (ncol > 0)
     LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, g->stream>>>(
-                             stage, cnt, (const uint64_t*)off.p, ncol, (float2*)ep.p));
+                             stage, cnt, (const uint64_t*)g->off.p, ncol, (float2*)g->ep.p));
   CK(cudaGetLastError());
   T.prof.finish();
   CK(timed_sync(g->stream));
-  dfree(g, g->off);
-  dfree(g, g->ep);
-  g->off = off;
-  g->ep = ep;
   g->n = n;
   stats.n_out = n;
   g->stats = stats;

@@ -18,7 +18,7 @@
 // endpoint is the same fp64 expression rounded once to fp32.
 //
 // One thread per column; a block is a tile of RT_X x RT_Y columns (a warp = 32 consecutive
-// columns of a row) and walks the tile's shape list (host-binned, conservative); every lane
+// columns of a row) and walks the tile's shape list (binned on the device, conservative); every lane
 // reads the same shape (broadcast load).  The unions live in per-thread local memory.
 // Results go to a [t][column] staging array, then the scan and compact_kernel (pass2.cuh).
 #pragma once
@@ -40,7 +40,7 @@ struct RasterArgs {
   int nbox;
   const double* box;           // [nbox][6] x0, x1, y0, y1, z0, z1
   const int32_t* box_sign;
-  const int64_t* tile_off;     // [ntiles + 1]
+  const uint64_t* tile_off;    // [ntiles + 1]
   const int32_t* tile_ids;     // shape ids: sphere k -> k, box k -> nsph + k
   int ntx;                     // tiles per tile row
   float2* stage;               // [RS_OUT][ncol]
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
   double2 P[RS_CAP], N[RS_CAP];
   int np = 0, nn = 0;
   bool ovf = false;
-  for (int64_t t = A.tile_off[tile]; t < A.tile_off[tile + 1]; ++t) {
+  for (uint64_t t = A.tile_off[tile]; t < A.tile_off[tile + 1]; ++t) {
     const int id = A.tile_ids[t];
     double lo, hi;
     int sg;
@@ -165,6 +165,56 @@ __global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
   }
   A.cnt[c] = k;
   if (ovf) atomicOr(A.flags, 1u);
+}
+
+// ---- tile binning on the device: every shape's conservative tile range, a count per tile, the
+// scan (host helper), then the fill; the order of ids inside a tile is arbitrary (the per-column
+// unions do not depend on it)
+struct RasterBin {
+  int nx, nrows, y0, ntx, nsph, nshape;
+  const double* sph;
+  const double* box;
+};
+
+__device__ __forceinline__ bool rs_tile_range(const RasterBin& B, int id, int& t0, int& t1, int& u0, int& u1) {
+  double xa, xb, ya, yb;
+  if (id < B.nsph) {
+    const double* q = B.sph + 4 * (size_t)id;
+    xa = q[0] - q[3]; xb = q[0] + q[3]; ya = q[1] - q[3]; yb = q[1] + q[3];
+  } else {
+    const double* q = B.box + 6 * (size_t)(id - B.nsph);
+    xa = q[0]; xb = q[1]; ya = q[2]; yb = q[3];
+  }
+  const double ia = floor(xa - 0.5) - 1, ib = ceil(xb - 0.5) + 1;
+  const double ja = floor(ya - 0.5) - 1 - B.y0, jb = ceil(yb - 0.5) + 1 - B.y0;
+  if (!(ib >= 0 && ia <= B.nx - 1 && jb >= 0 && ja <= B.nrows - 1)) return false;
+  t0 = (int)fmax(0.0, ia) / RT_X;
+  t1 = (int)fmin((double)B.nx - 1, ib) / RT_X;
+  u0 = (int)fmax(0.0, ja) / RT_Y;
+  u1 = (int)fmin((double)B.nrows - 1, jb) / RT_Y;
+  return true;
+}
+
+__global__ void raster_bin_count(RasterBin B, uint32_t* __restrict__ cnt) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= B.nshape) return;
+  int t0, t1, u0, u1;
+  if (!rs_tile_range(B, id, t0, t1, u0, u1)) return;
+  for (int u = u0; u <= u1; ++u)
+    for (int t = t0; t <= t1; ++t) atomicAdd(cnt + (int64_t)u * B.ntx + t, 1u);
+}
+
+__global__ void raster_bin_fill(RasterBin B, const uint64_t* __restrict__ off, uint32_t* __restrict__ cur,
+                                int32_t* __restrict__ ids) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= B.nshape) return;
+  int t0, t1, u0, u1;
+  if (!rs_tile_range(B, id, t0, t1, u0, u1)) return;
+  for (int u = u0; u <= u1; ++u)
+    for (int t = t0; t <= t1; ++t) {
+      const int64_t tile = (int64_t)u * B.ntx + t;
+      ids[off[tile] + atomicAdd(cur + tile, 1u)] = id;
+    }
 }
 
 }  // namespace dexel
