@@ -93,7 +93,7 @@ struct LvArgs {
   int64_t nlist;
 };
 
-constexpr int LV_T = 128;
+constexpr int LV_T = 64;
 constexpr int LV_D = 8;      // pieces per thread in the cp.async ring
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -126,7 +126,7 @@ struct LvTab {
 };
 
 template <int LMAX>
-__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 3 : 4) levels_kernel(LvArgs A) {
+__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs A) {
   constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
   __shared__ __align__(16) float Hs[257 * HS];   // h(kappa, k0 + k), NaN beyond R or out of reach;
                                                   // row R+1: all NaN (the "null piece")
