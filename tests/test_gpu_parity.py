@@ -625,3 +625,27 @@ def test_rasterize_shapes_errors(dx):
     dx.dexel_rasterize_shapes(g, 0.0, 64.0)   # no shapes: the empty solid
     assert g.size() == 0
     g.close()
+
+
+# ---------------------------------------------------------------- tri-dexel offsets (NEXT #4)
+@pytest.mark.parametrize("cfg,op,r", [("C1", "dilate", 3.0), ("C2", "shell", 4.0), ("C2", "erode", 4.0)])
+def test_tridexel_buffers_match_oracle(dx, cfg, op, r):
+    """Tri-dexel: each of the three buffers is rasterised bitwise like the host generator on the
+    permuted shapes, and its offset matches the oracle's op on that buffer's input."""
+    from paper_1804_08968_b200.tridexel import AXES, TriDexel, permute_shapes
+    n, zmin, zmax, sph, ss, box, bs = G.shape_config(cfg)
+    td = TriDexel.from_shapes(n, zmin, zmax, sph, ss, box, bs)
+    out = td.shell(r, r) if op == "shell" else getattr(td, op)(r)
+    for a in AXES:
+        s2, b2 = permute_shapes(a, sph, box)
+        host = G.shapes(n, n, zmin, zmax, spheres=s2[ss > 0], voids=s2[ss < 0], boxes=b2[bs > 0], box_voids=b2[bs < 0])
+        o_in, e_in = td.buf[a].download()
+        assert np.array_equal(o_in.astype(np.uint64), host.off.astype(np.uint64)) and np.array_equal(e_in, host.ep)
+        cols = sample_columns(n, n, 400, 2, 2, seed=11)
+        ref = O.shell(host, r, r, cols=cols) if op == "shell" else getattr(O, op)(host, r, cols=cols)
+        o, e = out.buf[a].download()
+        oo, zz = take_columns(o, e, cols)
+        res = compare(oo, zz, ref.off, ref.z, 1e-4)
+        assert res["ok"], (a, op, r, res)
+    td.close()
+    out.close()
