@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--op", default=None, choices=[None, "dilate", "erode", "shell", "dilate_slices", "erode_slices",
-                                                   "shell_slices", "rasterize"])
+                                                   "shell_slices", "rasterize", "tridexel_dilate", "tridexel_erode",
+                                                   "tridexel_shell"])
     ap.add_argument("--r", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -455,6 +456,62 @@ def run_b200(a, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_tridexel(a, rank, world):
+    """Tri-dexel offsets: the config's solid rasterised into three axis buffers
+    (setup, untimed); a step = the op on all three buffers (one stream, CUDA events).  Replicas
+    only: under torchrun every rank runs its own copy and rank 0 reports its own time."""
+    import torch
+
+    import dexelgen as G
+    import paper_1804_08968_b200 as dx
+    from paper_1804_08968_b200.tridexel import AXES, TriDexel
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    n, zmin, zmax, sph, ssg, box, bsg = G.shape_config(a.config)
+    td = TriDexel.from_shapes(n, zmin, zmax, sph, ssg, box, bsg, device=dev, stream=stream.cuda_stream)
+    out = td.like()
+    op = a.op[len("tridexel_"):]
+
+    def step():
+        if op == "shell":
+            td.shell(a.r, a.r, out)
+        else:
+            getattr(td, op)(a.r, out)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    launches = 0
+    for _ in range(a.steps):
+        step()
+        launches += sum(out.buf[x].stats()["launches"] for x in AXES)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    ncol = 3 * n * n
+    line = {"metric": metric_name(a.op), "value": ncol / (ms / 1e3), "unit": "columns/s", "n_gpus": 1,
+            "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, rasterised on the GPU into three axis buffers)",
+            "config": {"workload": f"{a.config} {a.op} r={a.r}", "grid": f"3 x {n}x{n}", "r": a.r,
+                       "n_in": int(td.size()), "n_out": int(out.size())},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    td.close()
+    out.close()
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -462,6 +519,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         run_reference(a, rank, world)
+    elif a.op.startswith("tridexel_"):
+        run_tridexel(a, rank, world)
     else:
         run_b200(a, rank, world, local_rank)
 
