@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -70,16 +71,6 @@ struct dexel_grid_s {
   unsigned char* pin = nullptr;   // pinned host scratch for the small device->host readbacks
   // capacity hints carried between ops (grown on overflow)
   int lev_cap = 0, p2_acc = 0, p1_cap = 0;
-  // device-memory budget for row bands, queried once and kept (a driver query per op costs
-  // 0.2-11 ms under contention, e.g. with a clock sampler); cleared when an op runs out of memory
-  size_t band_budget = 0;
-  // workspace: an op's large temporaries (band slot arrays, staging) stay allocated on the
-  // handle and are reused by size by later ops; freeing them to the stream-ordered pool and
-  // allocating again fragments the pool once other allocations (e.g. a re-upload) land in
-  // the freed blocks, and the pool then remaps tens of GB per op (measured: 150-900 ms)
-  std::vector<Buf> ws;
-  std::vector<char> ws_busy;
-  size_t ws_bytes = 0;
   // the previous input CSR after a re-upload: the next upload of a similar size fills it
   // instead of allocating (an upload must not touch the current contents until validated)
   Buf spare_off, spare_ep;
@@ -193,8 +184,47 @@ struct Prof {
   ~Prof() { finish(); }
 };
 
-// RAII for temporaries of one op
+// Device workspace: an op's large temporaries (band slot arrays, staging) stay allocated and
+// are reused by size by later ops of any handle on the device; freeing them to the
+// stream-ordered pool and allocating again fragments the pool once other allocations (e.g. a
+// re-upload) land in the freed blocks, and the pool then remaps tens of GB per op (measured:
+// 150-900 ms).  A block released on one stream and taken on another is ordered by an event.
+// Idle blocks are freed when the device's last handle is destroyed, or on out-of-memory.
+// The band budget lives here too (queried once per device: a driver query per op costs
+// 0.2-11 ms under contention, and one budget for all handles keeps the block sizes shared).
+struct WsEntry {
+  Buf b;
+  bool busy = false;
+  cudaEvent_t ev = nullptr;      // recorded on the stream that last released the block
+  cudaStream_t last = nullptr;
+};
+struct DevWs {
+  std::mutex mu;
+  std::vector<WsEntry> e;        // (indices are stable: freed entries keep an empty Buf)
+  int handles = 0;
+  size_t band_budget = 0;
+};
+DevWs& dev_ws(int device) {
+  static DevWs w[64];
+  return w[device & 63];
+}
 constexpr size_t WS_MIN = (size_t)32 << 20;   // temporaries from this size on use the workspace
+
+// free the idle blocks of a device's workspace, ordered after their last users on stream st
+void ws_trim_idle(dexel_grid g) {
+  DevWs& W = dev_ws(g->d.device);
+  std::lock_guard<std::mutex> lk(W.mu);
+  for (auto& e : W.e)
+    if (!e.busy && e.b.p) {
+      if (e.ev && e.last != g->stream) cudaStreamWaitEvent(g->stream, e.ev, 0);
+      dfree(g, e.b);
+      if (e.ev) cudaEventDestroy(e.ev);
+      e.ev = nullptr;
+      e.last = nullptr;
+    }
+}
+
+// RAII for temporaries of one op
 
 struct Temps {
   dexel_grid g;
@@ -209,32 +239,52 @@ struct Temps {
   ~Temps() {
     prof.finish();
     for (auto& b : bufs) dfree(g, b);
-    for (int w : wsi) g->ws_busy[w] = 0;
+    while (!wsi.empty()) release_ws(0);
+  }
+  void release_ws(size_t t) {   // hand block wsi[t] back, ordered after this op's stream work
+    DevWs& W = dev_ws(g->d.device);
+    std::lock_guard<std::mutex> lk(W.mu);
+    WsEntry& e = W.e[wsi[t]];
+    e.busy = false;
+    if (!e.ev) cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming);
+    if (e.ev) cudaEventRecord(e.ev, g->stream);
+    e.last = g->stream;
+    wsi.erase(wsi.begin() + t);
   }
   dexel_status get(size_t bytes, void** p) {
     if (bytes >= WS_MIN) {   // a free workspace block of about this size (at most 1/4 larger)
-      int best = -1;
-      for (int w = 0; w < (int)g->ws.size(); ++w)
-        if (!g->ws_busy[w] && g->ws[w].bytes >= bytes && g->ws[w].bytes - bytes <= bytes / 4 &&
-            (best < 0 || g->ws[w].bytes < g->ws[best].bytes))
-          best = w;
-      if (best < 0) {
-        Buf b;
-        dexel_status s = dalloc(g, b, bytes);
-        if (s == DEXEL_ENOMEM) {   // drop the idle workspace and retry once
-          trim_idle();
-          g_err.clear();
-          s = dalloc(g, b, bytes);
+      DevWs& W = dev_ws(g->d.device);
+      {
+        std::lock_guard<std::mutex> lk(W.mu);
+        int best = -1;
+        for (int w = 0; w < (int)W.e.size(); ++w)
+          if (!W.e[w].busy && W.e[w].b.p && W.e[w].b.bytes >= bytes && W.e[w].b.bytes - bytes <= bytes / 4 &&
+              (best < 0 || W.e[w].b.bytes < W.e[best].b.bytes))
+            best = w;
+        if (best >= 0) {
+          WsEntry& e = W.e[best];
+          e.busy = true;
+          if (e.ev && e.last != g->stream) cudaStreamWaitEvent(g->stream, e.ev, 0);
+          wsi.push_back(best);
+          *p = e.b.p;
+          return DEXEL_OK;
         }
-        if (s) return s;
-        g->ws.push_back(b);
-        g->ws_busy.push_back(0);
-        g->ws_bytes += b.bytes;
-        best = (int)g->ws.size() - 1;
       }
-      g->ws_busy[best] = 1;
-      wsi.push_back(best);
-      *p = g->ws[best].p;
+      Buf b;
+      dexel_status s = dalloc(g, b, bytes);
+      if (s == DEXEL_ENOMEM) {   // drop the idle workspace and retry once
+        ws_trim_idle(g);
+        g_err.clear();
+        s = dalloc(g, b, bytes);
+      }
+      if (s) return s;
+      std::lock_guard<std::mutex> lk(W.mu);
+      WsEntry e;
+      e.b = b;
+      e.busy = true;
+      W.e.push_back(e);
+      wsi.push_back((int)W.e.size() - 1);
+      *p = b.p;
       return DEXEL_OK;
     }
     Buf b;
@@ -247,20 +297,18 @@ struct Temps {
   void release(void* p) {
     for (auto& b : bufs)
       if (b.p == p) dfree(g, b);
-    for (size_t t = 0; t < wsi.size(); ++t)
-      if (g->ws[wsi[t]].p == p) {
-        g->ws_busy[wsi[t]] = 0;
-        wsi.erase(wsi.begin() + t);
+    for (size_t t = 0; t < wsi.size(); ++t) {
+      bool hit;
+      {
+        DevWs& W = dev_ws(g->d.device);
+        std::lock_guard<std::mutex> lk(W.mu);
+        hit = W.e[wsi[t]].b.p == p;
+      }
+      if (hit) {
+        release_ws(t);
         break;
       }
-  }
-  // free the workspace blocks no op holds (their slots stay in the vector as empty entries)
-  void trim_idle() {
-    for (size_t w = 0; w < g->ws.size(); ++w)
-      if (!g->ws_busy[w] && g->ws[w].p) {
-        g->ws_bytes -= g->ws[w].bytes;
-        dfree(g, g->ws[w]);
-      }
+    }
   }
 };
 
@@ -773,8 +821,8 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   // a grid whose whole extended slot set is small (under 1 GiB) is one band without asking the
   // driver (cudaMemGetInfo costs 0.2-1.5 ms, a large share of a small op)
   const size_t whole = row_bytes * (size_t)(src->nrows + 2 * Rmax);
-  if (whole > ((size_t)1 << 30) && src->band_budget) {
-    budget = src->band_budget;
+  if (whole > ((size_t)1 << 30) && dev_ws(src->d.device).band_budget) {
+    budget = dev_ws(src->d.device).band_budget;
   } else if (whole > ((size_t)1 << 30)) {
     // free device memory plus what the stream-ordered pool holds but does not use (freed
     // temporaries of earlier ops stay reserved: the release threshold is kept at max)
@@ -792,7 +840,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       }
       budget = std::min(budget, (fr + pooled) / 2);
     }
-    src->band_budget = budget;
+    dev_ws(src->d.device).band_budget = budget;
   }
   int band = (int)std::max<int64_t>(64, (int64_t)(budget / std::max<size_t>(row_bytes, 1)) - 2 * Rmax);
   if (const char* e = std::getenv("DEXEL_BAND_ROWS")) band = std::max(1, std::atoi(e));   // testing override
@@ -911,7 +959,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
 // an op that ran out of device memory drops the cached band budget (the next op re-queries)
 dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst, bool slices = false) {
   const dexel_status s = run_op_impl(op, src, r_a, r_b, dst, slices);
-  if (s == DEXEL_ENOMEM && src) src->band_budget = 0;
+  if (s == DEXEL_ENOMEM && src) dev_ws(src->d.device).band_budget = 0;
   return s;
 }
 
@@ -983,6 +1031,11 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
     return s;
   }
   CK(cudaMemsetAsync(g->off.p, 0, sizeof(uint64_t) * (g->ncol + 1), g->stream));
+  {
+    DevWs& W = dev_ws(g->d.device);
+    std::lock_guard<std::mutex> lk(W.mu);
+    ++W.handles;
+  }
   *out = g;
   return DEXEL_OK;
 }
@@ -1397,7 +1450,16 @@ void dexel_destroy(dexel_grid g) {
     dfree(g, g->hoff[q]);
     dfree(g, g->hep[q]);
   }
-  for (auto& b : g->ws) dfree(g, b);
+  {
+    DevWs& W = dev_ws(g->d.device);
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(W.mu);
+      last = --W.handles == 0;
+      if (last) W.band_budget = 0;
+    }
+    if (last) ws_trim_idle(g);   // the device's last handle: its workspace goes too
+  }
   dfree(g, g->spare_off);
   dfree(g, g->spare_ep);
   cudaStreamSynchronize(g->stream);
