@@ -490,9 +490,11 @@ struct P1Fam {
   bool has_out;
   float plo, phi;   // pending piece of the domination filter
   int pk;
+  const float2* trow;   // the threshold-table row of pk (row 17: no pending piece)
 };
 
-__device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int jr, int i, bool out_ok) {
+__device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int jr, int i, bool out_ok,
+                                            const float2* thr) {
   // lanes without output store into a spill cell (slot cap, never read)
   F.zb = P.z + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
   F.kb = P.k + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
@@ -503,6 +505,7 @@ __device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int j
   F.has_out = out_ok;
   F.plo = F.phi = 0.f;
   F.pk = KNONE;
+  F.trow = thr + 17 * 32;
 }
 
 // a piece [zstart, z] at level kap closed (closed == true): the domination filter against the
@@ -510,7 +513,7 @@ __device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int j
 __device__ __forceinline__ void p1_fam_step(P1Fam& F, bool closed, float zstart, float z, int kap,
                                             const float2* thr) {
   const bool hp = F.pk != KNONE;
-  const float2 th = thr[min(F.pk, 17) * 32 + (kap & 31)];
+  const float2 th = F.trow[kap & 31];
   const bool drop_new = z - F.phi <= th.x;
   const bool drop_pend = zstart - F.plo <= th.y;
   const bool wr = closed && hp && !drop_new && !drop_pend;
@@ -521,6 +524,7 @@ __device__ __forceinline__ void p1_fam_step(P1Fam& F, bool closed, float zstart,
   F.plo = take ? zstart : F.plo;
   F.phi = take ? z : F.phi;
   F.pk = take ? kap : F.pk;
+  F.trow = take ? thr + (kap & 31) * 32 : F.trow;   // (kap <= 16 whenever a piece is taken)
 }
 
 // flush the pending piece, store the count, list an overflowing column for list mode
@@ -615,8 +619,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
   const bool out_ok = i < src.nx;
   const int64_t c = (int64_t)jr * src.nx + i;
   P1Fam FS, FC;
-  p1_fam_init(FS, PS, jr, i, out_ok);
-  p1_fam_init(FC, PC, jr, i, out_ok);
+  p1_fam_init(FS, PS, jr, i, out_ok, thr_s);
+  p1_fam_init(FC, PC, jr, i, out_ok, thr_c);
   const int pp = lane + R;
   const int shr = pp < 32 ? pp : pp - 32;
   const int shl = pp >= 31 ? pp - 31 : 31 - pp;
