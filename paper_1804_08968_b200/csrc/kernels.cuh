@@ -625,15 +625,22 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
   const int shr = pp < 32 ? pp : pp - 32;
   const int shl = pp >= 31 ? pp - 31 : 31 - pp;
   const bool rlow = pp < 32, lhigh = pp >= 31;
-  auto nearest2 = [&](uint32_t m0, uint32_t m1) -> int {
-    const uint32_t rw = __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr) | 0x80000000u;
+  // this lane's two 32-bit windows of a 64-bit window mask: bits p .. p+31 (right) and
+  // p-31 .. p with bit p on top (left)
+  auto win_r = [&](uint32_t m0, uint32_t m1) { return __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr); };
+  auto win_l = [&](uint32_t m0, uint32_t m1) {
     const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
-    const uint32_t lw = (lhigh ? la : lb) | 1u;
-    const int d = min(__clz(lw), __ffs(rw) - 1);
+    return lhigh ? la : lb;
+  };
+  // nearest set bit from the windows (a sentinel at distance 31 > R keeps both non-zero)
+  auto nearest_w = [&](uint32_t rw, uint32_t lw) -> int {
+    const int d = min(__clz(lw | 1u), __ffs(rw | 0x80000000u) - 1);
     return d <= R ? d : KNONE;
   };
+  // C's mask is G & ~M: its windows are ~window(M) & window(G), window(G) fixed for the sweep
+  const uint32_t gr = win_r(G[0], G[1]), gl = win_l(G[0], G[1]);
   uint32_t M0 = 0u, M1 = 0u;                   // S activity of the window (warp-uniform)
-  int kap = KNONE, kapc = nearest2(G[0], G[1]);
+  int kap = KNONE, kapc = nearest_w(gr, gl);
   float zstart = 0.f, zstartc = src.zlo;
   auto sweep = [&](auto stg) {
     for (;;) {
@@ -653,8 +660,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
         }
       }
       const float z = keyf(zk);
-      const int knew = nearest2(M0, M1);
-      const int knewc = nearest2(G[0] & ~M0, G[1] & ~M1);
+      const uint32_t mr = win_r(M0, M1), ml = win_l(M0, M1);
+      const int knew = nearest_w(mr, ml);
+      const int knewc = nearest_w(gr & ~mr, gl & ~ml);
       const bool chg = knew != kap, chgc = knewc != kapc;
       // an event changes kappa only for lanes within R of its column: steps where no lane of
       // the warp changes (often: halo events) skip the filter / emission half (warp-uniform)
