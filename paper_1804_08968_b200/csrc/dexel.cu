@@ -685,8 +685,7 @@ template <int OP, int TT>
 void launch_pass2_t(const LevelSlots& A, const LevelSlots& B, int nx, int row0, int nrows, float zlo, float zhi,
                     const P2Out& O, cudaStream_t st) {
   const int acc = O.acc;
-  const int64_t n = (int64_t)nrows * nx;
-  const unsigned blocks = (unsigned)((n + TT - 1) / TT);
+  const unsigned blocks = (unsigned)((int64_t)((nx + TT - 1) / TT) * nrows);   // (column tiles) x rows
   if (blocks == 0) return;
   const size_t smem = pass2_smem_bytes(OP, acc, TT);
   if (smem > 48 * 1024)

@@ -176,10 +176,15 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
                                                    unsigned* flags) {
   extern __shared__ __align__(16) float2 p2_smem[];
   const int tid = threadIdx.x;
-  const int64_t cl = (int64_t)blockIdx.x * T + tid;
-  if (cl >= (int64_t)nrows_out * nx) return;
+  // column-tile-major block order: consecutive blocks are consecutive rows of one tile of T
+  // columns, so the blocks reading a level list (output rows j +- k) run close together in time
+  // and the list is read from L2 (row-major order put them ~2R rows x nx columns apart)
+  const int tile = (int)(blockIdx.x / (unsigned)nrows_out), jr = (int)(blockIdx.x % (unsigned)nrows_out);
+  const int i = tile * T + tid;
+  if (i >= nx) return;
+  const int64_t cl = (int64_t)jr * nx + i;
   const int64_t c = cbase + cl;
-  const int i = (int)(cl % nx), jg = row0 + (int)(cl / nx);
+  const int jg = row0 + jr;
   unsigned need = 0;
   Acc U{p2_smem + tid, 0};
   float2* scratch = p2_smem + (size_t)acc * T + tid;     // [P2_R][T]
