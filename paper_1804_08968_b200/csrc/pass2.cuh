@@ -38,17 +38,21 @@ struct Acc {
 };
 
 template <int T>
-__device__ __forceinline__ void acc_insert(Acc& A, int& p, float a, float b, int cap, unsigned* need) {
-  // p: first index with v[p].y >= a (monotone over one list, since the list's starts increase)
-  while (p < A.n && A.v[p * T].y < a) ++p;
+__device__ __forceinline__ void acc_insert(Acc& A, int& p, float2& w, float a, float b, int cap, unsigned* need) {
+  // p: first index with v[p].y >= a (monotone over one list, since the list's starts increase);
+  // w caches v[p] (valid while p < n), so an element covered at the cursor costs no load
+  while (p < A.n && w.y < a) {
+    ++p;
+    if (p < A.n) w = A.v[p * T];
+  }
   if (p < A.n) {
-    const float2 w = A.v[p * T];
     if (w.x <= a && b <= w.y) return;                 // covered
     if (w.x <= b) {                                   // overlaps [w.x, w.y]: merge the run p..q
       int q = p;
       float e = fmaxf(b, w.y);
       while (q + 1 < A.n && A.v[(q + 1) * T].x <= e) { ++q; e = fmaxf(e, A.v[q * T].y); }
-      A.v[p * T] = make_float2(fminf(a, w.x), e);
+      w = make_float2(fminf(a, w.x), e);
+      A.v[p * T] = w;
       const int drop = q - p;
       if (drop) {
         for (int t = q + 1; t < A.n; ++t) A.v[(t - drop) * T] = A.v[t * T];
@@ -60,7 +64,8 @@ __device__ __forceinline__ void acc_insert(Acc& A, int& p, float a, float b, int
   // disjoint from everything: insert before p (shift the tail right)
   if (A.n >= cap) { *need = max(*need, (unsigned)(A.n + 1)); return; }
   for (int t = A.n; t > p; --t) A.v[t * T] = A.v[(t - 1) * T];
-  A.v[p * T] = make_float2(a, b);
+  w = make_float2(a, b);
+  A.v[p * T] = w;
   ++A.n;
 }
 
@@ -90,8 +95,8 @@ __device__ __forceinline__ void p2_load(P2Batch& X, const float2* __restrict__ B
 // (Level sets are stored unclipped: each element is clipped to [zlo, zhi] here; clipping
 // commutes with the union.)
 template <int T>
-__device__ __forceinline__ void p2_insert(Acc& A, int& p, const P2Batch& X, float2* scratch, float zlo, float zhi,
-                                          int cap, unsigned* need) {
+__device__ __forceinline__ void p2_insert(Acc& A, int& p, float2& w, const P2Batch& X, float2* scratch, float zlo,
+                                          float zhi, int cap, unsigned* need) {
 #pragma unroll
   for (int u = 0; u < P2_R; ++u)
     if (u < X.n) scratch[u * T] = X.x[u];
@@ -99,7 +104,7 @@ __device__ __forceinline__ void p2_insert(Acc& A, int& p, const P2Batch& X, floa
   for (int u = 0; u < X.n; ++u) {
     const float2 v = scratch[u * T];
     const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
-    if (lo < hi) acc_insert<T>(A, p, lo, hi, cap, need);
+    if (lo < hi) acc_insert<T>(A, p, w, lo, hi, cap, need);
   }
 }
 
@@ -109,11 +114,12 @@ __device__ __forceinline__ void acc_insert_list(Acc& A, const P2Batch& X0, const
                                                 int64_t stride, float2* scratch, float zlo, float zhi, int cap,
                                                 unsigned* need) {
   int p = 0;
-  p2_insert<T>(A, p, X0, scratch, zlo, zhi, cap, need);
+  float2 w = A.n > 0 ? A.v[0] : make_float2(0.f, 0.f);
+  p2_insert<T>(A, p, w, X0, scratch, zlo, zhi, cap, need);
   for (int e0 = P2_R; e0 < nb; e0 += P2_R) {
     P2Batch X;
     p2_load<T>(X, B + (int64_t)e0 * stride, nb - e0, stride);
-    p2_insert<T>(A, p, X, scratch, zlo, zhi, cap, need);
+    p2_insert<T>(A, p, w, X, scratch, zlo, zhi, cap, need);
   }
 }
 
