@@ -498,6 +498,10 @@ __device__ __forceinline__ void p1_fam_init(P1Fam& F, const PieceSlots& P, int j
   // lanes without output store into a spill cell (slot cap, never read)
   F.zb = P.z + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
   F.kb = P.k + piece_index(P, jr, out_ok ? 0 : P.cap, out_ok ? i : 0);
+  // opaque per-lane base pointers: otherwise the compiler rebuilds them from the kernel
+  // parameter with 64-bit index arithmetic at every store (6 instructions instead of 3)
+  asm("mov.b64 %0, %0;" : "+l"(F.zb));
+  asm("mov.b64 %0, %0;" : "+l"(F.kb));
   F.zstep = out_ok ? (uint32_t)P.nx : 0u;
   F.wlim = (uint32_t)P.cap * F.zstep;   // the spill cell
   F.woff = 0;
