@@ -220,8 +220,10 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
       const float4 v = hrow[j];
       hv[4 * j] = v.x; hv[4 * j + 1] = v.y; hv[4 * j + 2] = v.z; hv[4 * j + 3] = v.w;
     }
-    // reach is monotone in k: skip when no lane's piece reaches this chunk (warp-uniform)
-    if (__all_sync(0xffffffffu, isnan(hv[0]))) continue;
+    // reach is monotone in k: skip when no lane's piece reaches this chunk (warp-uniform).
+    // (Level 0 is in reach of every real piece and t < mmax leaves some lane a real piece, so
+    // the first chunk never skips -- the test, which waits on the table load, runs from k0 > 0.)
+    if (k0 > 0 && __all_sync(0xffffffffu, isnan(hv[0]))) continue;
     bool pop = false;
 #pragma unroll
     for (int k = 0; k < LMAX; ++k) {
