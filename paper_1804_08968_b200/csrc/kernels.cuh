@@ -288,6 +288,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
       has_out = true;
     }
   }
+  // opaque per-lane base pointers (as in p1_fam_init: no per-store 64-bit index arithmetic)
+  asm("mov.b64 %0, %0;" : "+l"(zb));
+  asm("mov.b64 %0, %0;" : "+l"(kb));
   uint32_t M[NW];
 #pragma unroll
   for (int q = 0; q < NW; ++q) M[q] = 0u;          // window activity mask (warp-uniform)
