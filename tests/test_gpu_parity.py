@@ -649,3 +649,29 @@ def test_tridexel_buffers_match_oracle(dx, cfg, op, r):
         assert res["ok"], (a, op, r, res)
     td.close()
     out.close()
+
+
+def test_fused_shell_c5_bitwise_separate(dx):
+    """At full C5 size in the bench's configuration (3 bands), the fused shell pass 1 gives the
+    bitwise output of two separate sweeps."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, hashlib; sys.path.insert(0, %r)
+import numpy as np, dexelgen as G, paper_1804_08968_b200 as dx
+host = G.config("C5")
+src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
+dx.dexel_shell(src, 16.0, 16.0, dst)
+off, ep = dst.download()
+h = hashlib.sha256(); h.update(np.asarray(off).tobytes()); h.update(np.asarray(ep).tobytes())
+print("HASH", h.hexdigest(), dst.stats()["capacities"]["bands"])
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hashes = {}
+    for fuse in ("0", "1"):
+        env = dict(os.environ, DEXEL_NO_FUSE=fuse)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert out.returncode == 0, out.stdout + out.stderr
+        hashes[fuse] = [l.split()[1] for l in out.stdout.splitlines() if l.startswith("HASH")][0]
+    assert hashes["0"] == hashes["1"], hashes
