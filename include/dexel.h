@@ -213,6 +213,13 @@ typedef struct {
 } dexel_stats;
 dexel_status dexel_last_stats(dexel_grid g, dexel_stats* out);
 
+/* Release the device's idle op workspace: the large temporaries ops
+ * keep for reuse by later ops of any handle on the device (they are otherwise freed with the
+ * device's last handle).  Blocks in use by a running op are kept; waits for the last use of
+ * each freed block, and the device's stream-ordered pool is trimmed (its unused reserved memory
+ * goes back to the driver; synchronises the device).  The band budget is re-queried. */
+dexel_status dexel_trim_workspace(int device);
+
 /* Enable (1) / disable (0) per-kernel CUDA-event timing for later ops
  * (process-wide; adds one event pair per launch and one sync per op). */
 dexel_status dexel_set_timing(int on);

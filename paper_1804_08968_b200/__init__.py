@@ -24,7 +24,7 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_open", "dexel_close",
-           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_size",
+           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_trim_workspace", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows"]
@@ -83,6 +83,7 @@ def lib():
             "dexel_shell_slices": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
             "dexel_rasterize_shapes": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, ctypes.c_int, vp,
                                         vp, ctypes.c_int], ctypes.c_int),
+            "dexel_trim_workspace": ([ctypes.c_int], ctypes.c_int),
             "dexel_size": ([vp, u64p], ctypes.c_int),
             "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
             "dexel_pass1": ([vp, ctypes.c_float, ctypes.c_int, vp, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
@@ -310,6 +311,11 @@ def dexel_rasterize_shapes(g: Grid, zmin: float, zmax: float, sph=None, sph_sign
                                         ss.ctypes.data if len(ss) else None, len(box),
                                         box.ctypes.data if len(box) else None, bs.ctypes.data if len(bs) else None, 0))
     return g
+
+
+def trim_workspace(device: int = 0) -> None:
+    """Free the device's idle op workspace (kept for reuse by later ops otherwise)."""
+    _check(lib().dexel_trim_workspace(int(device)))
 
 
 def dexel_pass1(src: Grid, r: float, complement: bool = False):

@@ -1467,6 +1467,33 @@ void dexel_destroy(dexel_grid g) {
   delete g;
 }
 
+dexel_status dexel_trim_workspace(int device) {
+  g_err.clear();
+  if (device < 0 || device >= 64) return fail(DEXEL_EINVAL, "device out of range");
+  CK(cudaSetDevice(device));
+  DevWs& W = dev_ws(device);
+  std::lock_guard<std::mutex> lk(W.mu);
+  for (auto& e : W.e)
+    if (!e.busy && e.b.p) {
+      if (e.ev) cudaEventSynchronize(e.ev);   // its last user is done
+      if (e.b.freefn) e.b.freefn(e.b.p, e.b.bytes ? e.b.bytes : 16, device, nullptr, e.b.ctx);
+      else cudaFree(e.b.p);
+      e.b = Buf{};
+      if (e.ev) cudaEventDestroy(e.ev);
+      e.ev = nullptr;
+      e.last = nullptr;
+    }
+  W.band_budget = 0;   // (re-queried by the next op)
+  // the stream-ordered pool keeps freed memory reserved (release threshold: max): hand its
+  // unused part back to the driver too
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  return DEXEL_OK;
+}
+
 dexel_status dexel_set_timing(int on) {
   g_timing = on != 0;
   return DEXEL_OK;

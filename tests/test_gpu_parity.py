@@ -654,10 +654,15 @@ def test_tridexel_buffers_match_oracle(dx, cfg, op, r):
 def test_fused_shell_c5_bitwise_separate(dx):
     """At full C5 size in the bench's configuration (3 bands), the fused shell pass 1 gives the
     bitwise output of two separate sweeps."""
-    import hashlib
+    import gc
     import os
     import subprocess
     import sys
+
+    import torch
+    gc.collect()                      # (earlier tests' handles and cached blocks: the children
+    dx.trim_workspace(0)              # need the device's memory)
+    torch.cuda.empty_cache()
     code = r"""
 import sys, hashlib; sys.path.insert(0, %r)
 import numpy as np, dexelgen as G, paper_1804_08968_b200 as dx
