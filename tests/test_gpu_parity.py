@@ -680,3 +680,21 @@ print("HASH", h.hexdigest(), dst.stats()["capacities"]["bands"])
         assert out.returncode == 0, out.stdout + out.stderr
         hashes[fuse] = [l.split()[1] for l in out.stdout.splitlines() if l.startswith("HASH")][0]
     assert hashes["0"] == hashes["1"], hashes
+
+
+def test_trim_workspace_keeps_results(dx):
+    """dexel_trim_workspace frees the idle device workspace and trims the pool; later ops
+    allocate again and give bitwise the same output."""
+    host = G.config("C2")
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    dx.dexel_shell(src, 4.0, 4.0, dst)
+    a = dst.download()
+    dx.trim_workspace(0)
+    dx.dexel_shell(src, 4.0, 4.0, dst)
+    b = dst.download()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with pytest.raises(Exception):
+        dx.trim_workspace(-1)
+    src.close()
+    dst.close()
