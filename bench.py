@@ -256,14 +256,17 @@ def run_b200(a, rank, world, local_rank):
     ncol = host.ncol
     stream = torch.cuda.Stream(device=dev)
     dist = None
+    comm = None
+    from paper_1804_08968_b200.slabs import Slab, check_slabs, csr_rows, nccl_bootstrap
     if world > 1:
         import torch.distributed as dist_mod
         dist = dist_mod
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    from paper_1804_08968_b200.slabs import Slab, check_slabs
+        # the library's own NCCL communicator: every op exchanges its halo rows inside the C ABI
+        comm = nccl_bootstrap(rank, world, dev)
     R = int(np.floor(a.r))
     check_slabs(host.ny, world, R)
-    slab = Slab(host, rank, world, dev, stream.cuda_stream)
+    slab = Slab(host, rank, world, dev, stream.cuda_stream, transport="nccl" if world > 1 else "caller", comm=comm)
     src, dst = slab.src, slab.dst
     ncol_local = src.ncol   # columns this rank writes
     # rasterize: a step dexelises the config's analytic solid into the grid
@@ -276,10 +279,7 @@ def run_b200(a, rank, world, local_rank):
         if raster:
             dx.dexel_rasterize_shapes(src, zmin_w, zmax_w, sph, ssg, box, bsg)
             return
-        if world > 1:
-            with torch.cuda.stream(stream):
-                if not a.op.endswith("_slices"):   # (2D slice offsets read no other row)
-                    slab.refresh_halos(R)          # NCCL send/recv of the R boundary rows (data-path exchange)
+        # (y-slabs: the op exchanges its R halo rows with ranks g-1 / g+1 over NCCL internally)
         slab.op(a.op, a.r)
 
     def barrier():
@@ -380,24 +380,28 @@ def run_b200(a, rank, world, local_rank):
         e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
                "h2d_bytes_per_step": int(sph.nbytes + ssg.nbytes + box.nbytes + bsg.nbytes),
                "d2h_bytes_per_step": 8 * (ncol + 1) + 8 * nout, "ms_per_step": e_ms}
-    elif not a.no_e2e and world == 1:
-        h_off = torch.from_numpy(host.off.view(np.int64)).pin_memory()
-        h_ep = torch.from_numpy(host.ep).pin_memory()
+    elif not a.no_e2e:
+        # every rank: its slab's input CSR from pinned host memory, the (collective) op, its output
+        # slab back to pinned host memory -- through the C ABI, timed as the max over ranks
+        s_off, s_ep = csr_rows(host.off, host.ep, host.nx, slab.y0, slab.y1 - slab.y0)
+        n_in_local = int(s_off[-1])
+        h_off = torch.from_numpy(s_off.view(np.int64)).pin_memory()
+        h_ep = torch.from_numpy(s_ep).pin_memory()
         nout_cap = int(st["n_out"] * 1.1) + 1024
-        o_off = torch.empty(ncol + 1, dtype=torch.int64).pin_memory()
+        o_off = torch.empty(ncol_local + 1, dtype=torch.int64).pin_memory()
         o_ep = torch.empty(2 * nout_cap, dtype=torch.float32).pin_memory()
         L = dx.lib()
         ke = max(1, min(a.steps, 5))
 
         def e2e_step():
-            dx._check(L.dexel_upload(src.h, h_off.data_ptr(), h_ep.data_ptr(), host.n, 0))
+            dx._check(L.dexel_upload(src.h, h_off.data_ptr(), h_ep.data_ptr(), n_in_local, 0))
             step()
             n = dst.size()
             dx._check(L.dexel_download(dst.h, o_off.data_ptr(), o_ep.data_ptr(), nout_cap, 0))
             return n
 
         e2e_step()
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(ke):
@@ -409,9 +413,15 @@ def run_b200(a, rank, world, local_rank):
         # the library synchronises the stream around host copies, so wall-clock and events agree;
         # report the larger (host copies are stream-ordered on the same stream)
         e_ms = max(ev_ms, 1e3 * wall / ke)
+        byts = [8 * (ncol_local + 1) + 8 * n_in_local, 8 * (ncol_local + 1) + 8 * nout]
+        if dist is not None:
+            t = torch.tensor([e_ms] + byts, dtype=torch.float64, device=f"cuda:{dev}")
+            tm = t[:1].clone()
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            e_ms, byts = float(tm.item()), [int(v) for v in t[1:].tolist()]
         e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
-               "h2d_bytes_per_step": 8 * (ncol + 1) + 8 * host.n,
-               "d2h_bytes_per_step": 8 * (ncol + 1) + 8 * nout, "ms_per_step": e_ms}
+               "h2d_bytes_per_step": byts[0], "d2h_bytes_per_step": byts[1], "ms_per_step": e_ms}
 
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None
@@ -450,8 +460,14 @@ def run_b200(a, rank, world, local_rank):
     if world > 1:
         line["config"]["slab_rows"] = [slab.y0, slab.y1]
         line["config"]["halo_rows"] = R
+    if world > 1:
+        line["config"]["halo"] = "in-library NCCL send/recv (dexel_nccl_comm_init), overlapped with interior pass 1"
     if rank == 0:
         print(json.dumps(line), flush=True)
+    slab.close()
+    if comm:
+        torch.cuda.synchronize()
+        dx.nccl_comm_destroy(comm)
     if dist is not None:
         dist.destroy_process_group()
 
@@ -512,11 +528,37 @@ def run_tridexel(a, rank, world):
     out.close()
 
 
+def spawn_ranks(a):
+    """--gpus N > 1 without a launcher: re-exec this command under torchrun with N ranks (one per
+    GPU), or fail loudly when the box has fewer GPUs -- never bench one GPU as N."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} requested but this box has {have} CUDA device(s)"}), flush=True)
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} needs {a.gpus} GPUs, found {have}\n")
+        sys.exit(2)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")          # the NCCL init log shows all N ranks
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "b200" and "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        spawn_ranks(a)
+    if a.impl == "b200" and world > 1 and a.gpus != world:
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         run_reference(a, rank, world)
     elif a.op.startswith("tridexel_"):

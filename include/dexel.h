@@ -49,24 +49,50 @@ typedef struct {
   float z_lo, z_hi;     /* domain in the local frame, finite, z_lo < z_hi */
   int32_t device;       /* CUDA ordinal */
   void* stream;         /* cudaStream_t; NULL -> library-owned stream */
-  void* nccl_comm;      /* reserved, must be NULL: halos are exchanged by the caller (see below) */
+  void* nccl_comm;      /* ncclComm_t of the nranks slab owners (multi-GPU, see below) or NULL */
   int32_t rank, nranks; /* slab owner; 0,1 for a single GPU */
   int32_t y0, y1;       /* owned global rows [y0,y1); 0,ny for a single GPU */
 } dexel_desc;
 
 /* Multi-GPU y-slabs ("the 2D dilations can be
  * performed completely independently in every slice"): rank g owns rows
- * [y0, y1) of the global grid.  Pass 1 runs along x and is row-local; pass 2
- * runs along y and needs R = floor(r/s) rows of input beyond each slab
- * boundary.  The caller moves them between ranks (the reference binding uses
- * torch.distributed NCCL send/recv on device buffers):
- *   dexel_download_rows  packs owned boundary rows as a CSR slice,
- *   dexel_upload_halo    attaches a neighbour's rows below (side 0) or above
- *                        (side 1) the slab.
- * An op on a slab reads rows [y0 - halo0, y1 + halo1) and writes [y0, y1);
- * it fails with DEXEL_EINVAL if a halo is shorter than min(R, rows to the
- * grid edge).  Outputs of all slabs concatenated are bitwise equal to the
- * single-GPU output (per-column results do not depend on the partition). */
+ * [y0, y1) of the global grid; the ranks' slabs tile [0, ny) in rank order.
+ * Pass 1 runs along x and is row-local; pass 2 runs along y and needs
+ * R = floor(r/s) rows of INPUT beyond each slab boundary (the halo).  An op on a
+ * slab reads rows [y0 - hlo, y1 + hhi) and writes [y0, y1); outputs of all slabs
+ * concatenated are bitwise equal to the single-GPU output (per-column results do
+ * not depend on the partition).  Three ways to supply the halo rows:
+ *   - NCCL (desc.nccl_comm != NULL, nranks > 1): every op is COLLECTIVE -- all
+ *     ranks call it with the same radii -- and exchanges the halo rows itself:
+ *     ncclSend/ncclRecv with ranks g-1 and g+1 on an internal stream, interval
+ *     counts first (one host synchronisation: allocation sizes), then offsets
+ *     and endpoints, overlapped with pass 1 of the slab's own rows.  The first
+ *     op on a handle gathers every rank's [y0, y1) (ncclAllGather); a partition
+ *     that does not tile [0, ny), or a slab shorter than the rows a neighbour
+ *     needs from it, fails with DEXEL_EINVAL on every rank alike.  Bootstrap:
+ *     dexel_nccl_unique_id on one rank, broadcast the 128 bytes (e.g. with
+ *     torch.distributed), dexel_nccl_comm_init on every rank.
+ *   - loopback (dexel_link_slabs): slab handles of ONE process (one device or
+ *     peer devices) fetch their halo rows from the linked neighbour handles with
+ *     device copies -- the same pass-1 split and halo layout as NCCL (tests).
+ *   - caller-managed (nccl_comm NULL, not linked): the caller moves the rows,
+ *     dexel_download_rows packs owned boundary rows as a CSR slice and
+ *     dexel_upload_halo attaches a neighbour's rows below (side 0) or above
+ *     (side 1) the slab; an op fails with DEXEL_EINVAL if a halo is shorter than
+ *     min(R, rows to the grid edge). */
+
+/* NCCL bootstrap helpers (the library links the NCCL 2.28 that PyTorch bundles). */
+dexel_status dexel_nccl_unique_id(uint8_t id[128]);                 /* ncclGetUniqueId */
+/* ncclCommInitRank on `device` (collective over the nranks callers); *comm receives the
+ * ncclComm_t to put in dexel_desc.nccl_comm.  It must outlive the handles using it. */
+dexel_status dexel_nccl_comm_init(const uint8_t id[128], int nranks, int rank, int device, void** comm);
+dexel_status dexel_nccl_comm_destroy(void* comm);                   /* NULL-safe */
+
+/* Loopback halo transport: slabs[q] must be the handle of rank q of n (desc.rank = q,
+ * desc.nranks = n, nccl_comm NULL), all of one grid, rows tiling [0, ny) in order.
+ * Later ops on any of them fetch halo rows from the linked neighbours (which must hold their
+ * inputs and not be running ops at the time).  Destroying a handle unlinks it. */
+dexel_status dexel_link_slabs(dexel_grid* slabs, int n);
 
 /* Create an empty grid (all columns empty).  *out receives the handle. */
 dexel_status dexel_create(const dexel_desc* d, dexel_grid* out);
@@ -88,8 +114,11 @@ dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* en
  * along y: power dilation with weights r^2 - d^2), clipped to U.
  * r finite, >= 0; R = floor(r/spacing) <= 255.  src and dst must share the
  * geometry (EMISMATCH) and differ (EINVAL).  dst is replaced; on error it is
- * left empty.  Output is canonical and bitwise deterministic.  Synchronises
- * the stream up to three times (allocation sizes). */
+ * left empty.  Output is canonical and bitwise deterministic.  Host
+ * synchronisations: the op reads allocation sizes and capacity flags back from
+ * the device (DESIGN.md "Host synchronisations" lists them; a y-slab with an
+ * NCCL communicator adds one for the halo sizes).  The stream is otherwise not
+ * synchronised: the op's last kernels may still run when it returns. */
 dexel_status dexel_dilate(dexel_grid src, float r, dexel_grid dst);
 
 /* dst := E_r(src) = U \ D_r(U \ src).  Same rules. */
@@ -105,8 +134,9 @@ dexel_status dexel_shell(dexel_grid src, float r_out, float r_in, dexel_grid dst
  *   dexel_close: dst := E_r(D_r(src))   (fills gaps and holes narrower than 2r)
  * computed as two ops through an internal temporary handle on src's stream.  With the
  * neutral boundary (R6), open(S) <= S <= close(S) and both are idempotent up to
- * fp32 rounding.  Same argument rules as dexel_dilate; a y-slab handle (nranks > 1) returns
- * DEXEL_EINVAL (the intermediate needs a halo exchange: compose the ops instead). */
+ * fp32 rounding.  Same argument rules as dexel_dilate.  On y-slabs with an NCCL communicator the
+ * intermediate's halo rows are exchanged like any input (collective); other y-slab handles
+ * (loopback, caller-managed) return DEXEL_EINVAL (compose the ops with an exchange between). */
 dexel_status dexel_open(dexel_grid src, float r, dexel_grid dst);
 dexel_status dexel_close(dexel_grid src, float r, dexel_grid dst);
 

@@ -27,7 +27,8 @@ EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel
            "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_trim_workspace", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
-           "dexel_download_rows"]
+           "dexel_download_rows", "dexel_nccl_unique_id", "dexel_nccl_comm_init", "dexel_nccl_comm_destroy",
+           "dexel_link_slabs"]
 
 
 class DexelError(RuntimeError):
@@ -95,6 +96,10 @@ def lib():
             "dexel_set_timing": ([ctypes.c_int], ctypes.c_int),
             "dexel_upload_halo": ([vp, ctypes.c_int, vp, vp, ctypes.c_int, u64, ctypes.c_int], ctypes.c_int),
             "dexel_download_rows": ([vp, ctypes.c_int, ctypes.c_int, vp, vp, u64, u64p, ctypes.c_int], ctypes.c_int),
+            "dexel_nccl_unique_id": ([vp], ctypes.c_int),
+            "dexel_nccl_comm_init": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+            "dexel_nccl_comm_destroy": ([vp], ctypes.c_int),
+            "dexel_link_slabs": ([ctypes.POINTER(vp), ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -259,6 +264,34 @@ class Grid:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (ncclGetUniqueId) for dexel_nccl_comm_init; broadcast it to every rank."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().dexel_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid: bytes, nranks: int, rank: int, device: int) -> int:
+    """ncclCommInitRank through the library (collective): the ncclComm_t for Grid(..., nccl_comm=)."""
+    if len(uid) != 128:
+        raise ValueError("NCCL unique id must be 128 bytes")
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    c = ctypes.c_void_p()
+    _check(lib().dexel_nccl_comm_init(buf, int(nranks), int(rank), int(device), ctypes.byref(c)))
+    return c.value
+
+
+def nccl_comm_destroy(comm: Optional[int]) -> None:
+    _check(lib().dexel_nccl_comm_destroy(comm))
+
+
+def link_slabs(slabs) -> None:
+    """Loopback halo transport (dexel_link_slabs): slab handles of rank 0..n-1 of one process fetch
+    their halo rows from each other inside every op."""
+    arr = (ctypes.c_void_p * len(slabs))(*[g.h.value for g in slabs])
+    _check(lib().dexel_link_slabs(arr, len(slabs)))
 
 
 def set_timing(on: bool):

@@ -16,6 +16,24 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
+def nccl_dir() -> str:
+    """NCCL 2.28 as bundled with PyTorch (nvidia/nccl in site-packages): the same libnccl.so.2 the
+    process already maps when torch.distributed uses NCCL."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (expected site-packages/nvidia/nccl)")
+
+
+def nccl_flags() -> list:
+    d = nccl_dir()
+    lib = os.path.join(d, "lib")
+    return ["-I", os.path.join(d, "include"), "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+
+
 def nvcc() -> str:
     for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
@@ -34,7 +52,7 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT,
-               *[os.path.join(CSRC, s) for s in SOURCES]]
+               *[os.path.join(CSRC, s) for s in SOURCES], *nccl_flags()]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "dexel.h"
 #include "kernels.cuh"
 #include "levels.cuh"
@@ -78,6 +80,16 @@ struct dexel_grid_s {
   Buf hoff[2], hep[2];
   int hrows[2] = {0, 0};
   uint64_t hn[2] = {0, 0};
+  // halo transport: NCCL (desc.nccl_comm), loopback links to the
+  // neighbouring slab handles of one process (dexel_link_slabs), else caller-managed halos
+  // (dexel_upload_halo).  The exchange runs on its own stream; pass 1 of the slab's own rows
+  // does not wait for it, the halo rows' launches wait on ev_halo.
+  dexel_grid_s* link[2] = {nullptr, nullptr};
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_halo = nullptr;
+  bool halo_pending = false;
+  std::vector<int32_t> part;   // NCCL: every rank's slab rows (y0, y1), gathered on first use
+  Buf hdr;                     // NCCL: interval counts sent [0..1] / received [2..3]
 };
 
 namespace {
@@ -216,7 +228,10 @@ void ws_trim_idle(dexel_grid g) {
   std::lock_guard<std::mutex> lk(W.mu);
   for (auto& e : W.e)
     if (!e.busy && e.b.p) {
-      if (e.ev && e.last != g->stream) cudaStreamWaitEvent(g->stream, e.ev, 0);
+      // a caller allocator (e.g. torch's caching allocator) only orders the free on its own
+      // allocation stream: wait for the block's last user on the host before handing it back
+      if (e.ev && e.b.freefn) cudaEventSynchronize(e.ev);
+      else if (e.ev && e.last != g->stream) cudaStreamWaitEvent(g->stream, e.ev, 0);
       dfree(g, e.b);
       if (e.ev) cudaEventDestroy(e.ev);
       e.ev = nullptr;
@@ -353,29 +368,43 @@ dexel_status check_radius(float r, double s, int* R) {
 }
 
 // ---------------------------------------------------------------- pass 1
-void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int nrows_out, const PieceSlots& P,
-               int64_t nlist, const float* prune, cudaStream_t st) {
+// one pass-1 launch: main mode over slot rows [jr0, jr0 + nrows_out) of a band whose slot row 0
+// is extended row row0; list mode (nlist >= 0) over the listed tiles
+void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int jr0, int nrows_out,
+               const PieceSlots& P, int64_t nlist, const float* prune, cudaStream_t st) {
   const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune)
+#define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, jr0, nrows_out, P, nlist, prune)
   // (skipping sweep steps that change no lane's kappa pays from R = 8; measured)
-  // the ring-buffered emission variant (closed pieces parked in shared memory, filtered in
-  // batches) was faster for R < 8 until the inline filter became table-driven and branch-free;
-  // it is kept behind an experiment override (DEXEL_P1_RING_BELOW=R: use it below R)
-  static const int ring_below = [] {
-    const char* e = std::getenv("DEXEL_P1_RING_BELOW");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (R < ring_below && NW <= 2) p1_kernel<2, true><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
-  else if (NW <= 2 && R < 8)
-    p1_kernel<2, false, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, nrows_out, P, nlist, prune);
+  if (NW <= 2 && R < 8)
+    p1_kernel<2, false, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, jr0, nrows_out, P, nlist, prune);
   else if (NW <= 2) P1(2);
   else if (NW <= 3) P1(3);
   else if (NW <= 5) P1(5);
   else if (NW <= 9) P1(9);
   else P1(17);
 #undef P1
+}
+
+// Pass-1 launches of band rows [row0, row0 + nrows) (extended numbering), split so that the
+// slab's own rows go first and the halo rows -- still arriving on the exchange stream when
+// g->halo_pending -- wait for the exchange (g->ev_halo): the transfer overlaps the interior
+// pass 1.  f(jr0, count) launches slot rows [jr0, jr0 + count) of the band.
+template <class F>
+cudaError_t launch_rows_split(dexel_grid g, const SrcRows& src, int row0, int nrows, F&& f) {
+  const int own0 = src.rows[0], own1 = src.rows[0] + src.rows[1], r1 = row0 + nrows;
+  auto seg = [&](int a, int b) { if (b > a) f(a - row0, b - a); };
+  if (!g->halo_pending || (row0 >= own0 && r1 <= own1)) {
+    seg(row0, r1);
+    return cudaGetLastError();
+  }
+  seg(std::max(row0, own0), std::min(r1, own1));      // the slab's own rows: no wait
+  cudaError_t e = cudaStreamWaitEvent(g->stream, g->ev_halo, 0);
+  if (e != cudaSuccess) return e;
+  seg(row0, std::min(r1, own0));                      // halo rows below the slab
+  seg(std::max(row0, own1), r1);                      // halo rows above
+  return cudaGetLastError();
 }
 
 // Pass 1 over rows [row0, row0+nrows) of src: pieces into per-column slots (one launch);
@@ -405,6 +434,9 @@ dexel_status p1_slots(dexel_grid g, Temps& T, const SrcRows& src, int nrows, Pie
   const int64_t ncol = (int64_t)nrows * src.nx;
   const int ntiles = (src.nx + 31) / 32;
   dexel_status s;
+  // the kernels address a column's slots with 32-bit offsets (slot * nx)
+  if ((size_t)(P->cap + 1) * (size_t)src.nx >= ((size_t)1 << 32))
+    return fail(DEXEL_EOVERFLOW, "pass-1 slot offsets exceed 32 bits (grid too wide for the piece capacity)");
   const size_t nslot = (size_t)ncol * (P->cap + 1);
   if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&P->z))) return s;
   if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
@@ -436,7 +468,7 @@ dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
     if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
     if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
     T.prof.pre(K_P1LIST);
-    launch_p1(NW, src, R, complement, row0, nrows, *P, (int64_t)hf[2], prune, g->stream);
+    launch_p1(NW, src, R, complement, row0, 0, nrows, *P, (int64_t)hf[2], prune, g->stream);
     T.prof.post();
     CK(cudaGetLastError());
     // the list launch adds the arena columns' (filtered) counts to the total
@@ -456,10 +488,11 @@ dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
   if ((s = p1_setup(g, T, src, nrows, P))) return s;
   for (int attempt = 0; attempt < 8; ++attempt) {
     if ((s = p1_slots(g, T, src, nrows, P))) return s;
-    T.prof.pre(K_P1);
-    launch_p1(NW, src, R, complement, row0, nrows, *P, -1, prune, g->stream);
-    T.prof.post();
-    CK(cudaGetLastError());
+    CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
+      T.prof.pre(K_P1);
+      launch_p1(NW, src, R, complement, row0, jr0, cnt, *P, -1, prune, g->stream);
+      T.prof.post();
+    }));
     unsigned hf[3];
     unsigned long long tot = 0;
     {
@@ -487,15 +520,15 @@ dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, i
   if ((s = p1_setup(g, T, src, nrows, PB))) return s;
   if ((s = p1_slots(g, T, src, nrows, PA))) return s;
   if ((s = p1_slots(g, T, src, nrows, PB))) return s;
-  const int64_t warps = (int64_t)nrows * ((src.nx + 31) / 32);
-  const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
-  if (blocks > 0) {
+  CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
+    const int64_t warps = (int64_t)cnt * ((src.nx + 31) / 32);
+    const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
+    if (blocks == 0) return;
     T.prof.pre(K_P1);
-    if (R >= 8) p1_dual_kernel<true><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
-    else p1_dual_kernel<false><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, nrows, *PA, *PB, prune_a, prune_b);
+    if (R >= 8) p1_dual_kernel<true><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, jr0, cnt, *PA, *PB, prune_a, prune_b);
+    else p1_dual_kernel<false><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, jr0, cnt, *PA, *PB, prune_a, prune_b);
     T.prof.post();
-    CK(cudaGetLastError());
-  }
+  }));
   unsigned hf[2][4];
   unsigned long long tot[2] = {0, 0};
   {
@@ -543,13 +576,15 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
     }
   // capsule-domination table for the pass-1 filter: h(kappa, 0), rounded once to fp32
   // (DEXEL_NO_PRUNE=1 disables the filter)
-  std::vector<float> h0(n1);
+  // (+ one entry: the absolute part of the domination margin, 16 r 2^-24 >= 4 ulp(r), kernels.cuh)
+  std::vector<float> h0(n1 + 1);
   for (int a = 0; a < n1; ++a) h0[a] = (float)std::sqrt(std::max(0.0, rr - (double)a * a * s * s));
+  h0[n1] = (float)(16.0 * (double)r * std::ldexp(1.0, -24));
   dexel_status st;
-  if ((st = T.get(sizeof(float) * (h.size() + n1) + 16, (void**)out))) return st;
+  if ((st = T.get(sizeof(float) * (h.size() + n1 + 1) + 16, (void**)out))) return st;
   float* d0 = *out + h.size();
   CK(cudaMemcpyAsync(*out, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(d0, h0.data(), sizeof(float) * n1, cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(d0, h0.data(), sizeof(float) * (n1 + 1), cudaMemcpyHostToDevice, g->stream));
   CK(timed_sync(g->stream));  // the host vectors go out of scope
   const char* e = std::getenv("DEXEL_NO_PRUNE");
   *prune = (e && std::atoi(e)) ? nullptr : d0;
@@ -618,7 +653,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_cap, nullptr, 0};
     launch(A, ncol);
     CK(cudaGetLastError());
-    unsigned hf[2];
+    unsigned hf[3];
     unsigned long long hn = 0;
     {
       Readback rb{g};
@@ -628,8 +663,6 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
       rb.get(0, hf, sizeof(hf));
       rb.get(16, &hn, sizeof(hn));
     }
-    if (hf[0] > (unsigned)LV_OVF_CAP)
-      return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
     if (dbg) {
       unsigned long long hd[2];
       CK(cudaMemcpy(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost));
@@ -640,7 +673,12 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     }
     if (hf[1] <= ovf_cap) {
       if (hf[1] > 0) {   // overflow pass: the listed columns' lists, all of them, into the arena
-        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * (R + 1) * (LV_OVF_CAP + 1) + 16, (void**)&L->ovf_z)))
+        // arena lists of the most pieces any listed column has (a list never holds more)
+        L->ovf_cap = (int)std::max(hf[2], 1u);
+        if (L->ovf_cap > LV_CNT_MAX)
+          return fail(DEXEL_EOVERFLOW, "a column has more than " + std::to_string(LV_CNT_MAX) +
+                                           " pass-1 pieces (level lists are counted in 15 bits)");
+        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * (R + 1) * (L->ovf_cap + 1) + 16, (void**)&L->ovf_z)))
           return s;
         LvArgs B = A;
         B.L = *L;
@@ -648,22 +686,13 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
         B.nlist = hf[1];
         launch(B, hf[1]);
         CK(cudaGetLastError());
-        // a list that outgrows the arena (255) only shows there when the sweep popped back
-        // below the capacity in the main pass
-        Readback rb{g};
-        rb.add(0, flags, sizeof(unsigned));
-        CK(rb.wait());
-        unsigned f0 = 0;
-        rb.get(0, &f0, sizeof(f0));
-        if (f0 > (unsigned)LV_OVF_CAP)
-          return fail(DEXEL_EOVERFLOW, "a column has more than 255 intervals in one level set");
       }
       *n_lev += hn;   // (the overflow pass adds nothing to the count)
       break;
     }
     // too many long lists: a larger slot capacity pays
     T.release(L->z);
-    L->cap = std::min(LV_OVF_CAP, 2 * L->cap);
+    L->cap = std::min(LV_SLOT_MAX, 2 * L->cap);
     g->lev_cap = L->cap;
     if (attempt == 5) return fail(DEXEL_ECUDA, "level capacity sizing did not converge");
   }
@@ -724,9 +753,216 @@ bool same_geometry(const dexel_desc& a, const dexel_desc& b) {
 }
 
 void set_empty(dexel_grid g) {
+  g->n = 0;
+  if (!g->off.p) dalloc(g, g->off, sizeof(uint64_t) * (g->ncol + 1));
   if (g->off.p) cudaMemsetAsync(g->off.p, 0, sizeof(uint64_t) * (g->ncol + 1), g->stream);
   dfree(g, g->ep);
-  g->n = 0;
+}
+
+// ---------------------------------------------------------------- halo exchange (multi-GPU)
+#define NK(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess) return fail(DEXEL_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// the boundary slices a slab sends: rows [0, sr0) to rank g-1, rows [nrows - sr1, nrows) to g+1.
+// hdr[2 s] = intervals of slice s, hdr[2 s + 1] = its first interval (the offset the receiver
+// subtracts)
+__global__ void halo_header(const uint64_t* __restrict__ off, int64_t c_lo, int64_t c_hi0, int64_t c_end,
+                            uint64_t* __restrict__ hdr) {
+  hdr[0] = off[c_lo];
+  hdr[1] = 0;
+  hdr[2] = off[c_end] - off[c_hi0];
+  hdr[3] = off[c_hi0];
+}
+
+// received offsets (absolute in the sender's CSR) -> offsets of a CSR of their own
+__global__ void halo_rebase(uint64_t* __restrict__ o, uint64_t n, const uint64_t* __restrict__ base_dev,
+                            uint64_t base_host) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t b = base_dev ? *base_dev : base_host;
+  if (t <= n) o[t] -= b;
+}
+
+enum { HALO_CALLER = 0, HALO_NCCL = 1, HALO_LOOP = 2 };
+int halo_mode(const dexel_grid g) {
+  if (g->d.nranks <= 1) return HALO_CALLER;
+  if (g->d.nccl_comm) return HALO_NCCL;
+  if (g->link[0] || g->link[1]) return HALO_LOOP;
+  return HALO_CALLER;
+}
+
+dexel_status ensure_comm_stream(dexel_grid g) {
+  if (!g->comm) CK(cudaStreamCreateWithFlags(&g->comm, cudaStreamNonBlocking));
+  if (!g->ev_main) CK(cudaEventCreateWithFlags(&g->ev_main, cudaEventDisableTiming));
+  if (!g->ev_halo) CK(cudaEventCreateWithFlags(&g->ev_halo, cudaEventDisableTiming));
+  return DEXEL_OK;
+}
+
+// the exchange stream waits for everything queued on the handle's stream so far
+dexel_status comm_after_main(dexel_grid g) {
+  CK(cudaEventRecord(g->ev_main, g->stream));
+  CK(cudaStreamWaitEvent(g->comm, g->ev_main, 0));
+  return DEXEL_OK;
+}
+
+// a halo buffer of at least `bytes` (kept on the handle between ops; reallocated when too small or
+// more than twice too large).  Allocated on the handle's stream: call comm_after_main afterwards.
+dexel_status halo_buf(dexel_grid g, Buf& b, size_t bytes) {
+  if (b.p && b.bytes >= bytes && b.bytes <= 2 * bytes + 4096) return DEXEL_OK;
+  dfree(g, b);
+  return dalloc(g, b, bytes);
+}
+
+// NCCL: every rank's slab rows, gathered once per handle; the partition must tile [0, ny) in
+// rank order (every rank sees the same table, so every rank takes the same decisions below)
+dexel_status nccl_partition(dexel_grid g) {
+  if (!g->part.empty()) return DEXEL_OK;
+  ncclComm_t comm = (ncclComm_t)g->d.nccl_comm;
+  const int P = g->d.nranks;
+  int cnt = 0, rk = -1;
+  NK(ncclCommCount(comm, &cnt));
+  NK(ncclCommUserRank(comm, &rk));
+  if (cnt != P || rk != g->d.rank)
+    return fail(DEXEL_EINVAL, "nccl_comm has " + std::to_string(cnt) + " ranks (this is rank " + std::to_string(rk) +
+                                  "), the descriptor says rank " + std::to_string(g->d.rank) + " of " +
+                                  std::to_string(P));
+  Buf b;
+  dexel_status s = dalloc(g, b, sizeof(int32_t) * 2 * (P + 1));
+  if (s) return s;
+  const int32_t mine[2] = {g->d.y0, g->d.y1};
+  CK(cudaMemcpyAsync((int32_t*)b.p + 2 * P, mine, sizeof(mine), cudaMemcpyHostToDevice, g->stream));
+  if ((s = ensure_comm_stream(g)) || (s = comm_after_main(g))) { dfree(g, b); return s; }
+  NK(ncclAllGather((int32_t*)b.p + 2 * P, b.p, 2, ncclInt32, comm, g->comm));
+  std::vector<int32_t> part(2 * P);
+  CK(cudaMemcpyAsync(part.data(), b.p, sizeof(int32_t) * 2 * P, cudaMemcpyDeviceToHost, g->comm));
+  CK(timed_sync(g->comm));
+  ncclResult_t ae = ncclSuccess;
+  ncclCommGetAsyncError(comm, &ae);
+  if (ae != ncclSuccess) return fail(DEXEL_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(ae));
+  CK(cudaEventRecord(g->ev_main, g->comm));   // the handle's stream may free b only after the gather
+  CK(cudaStreamWaitEvent(g->stream, g->ev_main, 0));
+  dfree(g, b);
+  for (int q = 0; q < P; ++q) {
+    const bool ok = part[2 * q] < part[2 * q + 1] && (q == 0 ? part[0] == 0 : part[2 * q] == part[2 * q - 1]) &&
+                    (q + 1 < P || part[2 * q + 1] == g->d.ny);
+    if (!ok)
+      return fail(DEXEL_EINVAL, "the ranks' slabs [y0, y1) must tile [0, ny) in rank order (rank " + std::to_string(q) +
+                                    " has [" + std::to_string(part[2 * q]) + ", " + std::to_string(part[2 * q + 1]) + "))");
+  }
+  g->part = part;
+  return DEXEL_OK;
+}
+
+// Start the op's halo exchange (SURVEY 8(e) Option A): the R input rows beyond each
+// slab boundary come from ranks g-1 / g+1 into g->hoff/hep, on the exchange stream; g->ev_halo
+// marks their arrival (pass 1 of the halo rows waits on it, launch_rows_split).  Two phases,
+// because rows are ragged: the interval counts (one host synchronisation: allocation sizes), then
+// offsets and endpoints.  Sends read the slab's own CSR in place (contiguous row ranges).
+dexel_status halo_begin(dexel_grid g, int R) {
+  const int mode = halo_mode(g);
+  const int nx = g->d.nx, ny = g->d.ny, y0 = g->d.y0, y1 = g->d.y1;
+  const int need[2] = {std::min(R, y0), std::min(R, ny - y1)};
+  dexel_status s;
+  if ((s = ensure_comm_stream(g))) return s;
+  uint64_t recv_n[2] = {0, 0};
+  if (mode == HALO_NCCL) {
+    if ((s = nccl_partition(g))) return s;
+    const int P = g->d.nranks, me = g->d.rank;
+    // rank q sends min(R, ny - y0_q) rows down and min(R, y1_q) rows up: both must lie in its slab
+    for (int q = 0; q < P; ++q) {
+      const int qy0 = g->part[2 * q], qy1 = g->part[2 * q + 1], rows = qy1 - qy0;
+      if ((q > 0 && std::min(R, ny - qy0) > rows) || (q + 1 < P && std::min(R, qy1) > rows))
+        return fail(DEXEL_EINVAL, "slab of rank " + std::to_string(q) + " has " + std::to_string(rows) +
+                                      " rows < R = " + std::to_string(R) + ": its neighbours' halos would reach past it");
+    }
+    ncclComm_t comm = (ncclComm_t)g->d.nccl_comm;
+    const int peer[2] = {me - 1, me + 1 < P ? me + 1 : -1};
+    const int sr[2] = {peer[0] >= 0 ? std::min(R, ny - y0) : 0, peer[1] >= 0 ? std::min(R, y1) : 0};
+    if ((s = halo_buf(g, g->hdr, 8 * sizeof(uint64_t)))) return s;
+    uint64_t* hdr = (uint64_t*)g->hdr.p;
+    if ((s = comm_after_main(g))) return s;
+    halo_header<<<1, 1, 0, g->comm>>>((const uint64_t*)g->off.p, (int64_t)sr[0] * nx, (int64_t)(g->nrows - sr[1]) * nx,
+                                      g->ncol, hdr);
+    CK(cudaGetLastError());
+    NK(ncclGroupStart());
+    for (int q = 0; q < 2; ++q)
+      if (peer[q] >= 0) {
+        NK(ncclSend(hdr + 2 * q, 2, ncclUint64, peer[q], comm, g->comm));
+        NK(ncclRecv(hdr + 4 + 2 * q, 2, ncclUint64, peer[q], comm, g->comm));
+      }
+    NK(ncclGroupEnd());
+    uint64_t h[8];
+    CK(cudaMemcpyAsync(g->pin, hdr, sizeof(h), cudaMemcpyDeviceToHost, g->comm));
+    CK(timed_sync(g->comm));
+    std::memcpy(h, g->pin, sizeof(h));
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(comm, &ae);
+    if (ae != ncclSuccess) return fail(DEXEL_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(ae));
+    for (int q = 0; q < 2; ++q) {
+      recv_n[q] = peer[q] >= 0 ? h[4 + 2 * q] : 0;
+      if (need[q] && ((s = halo_buf(g, g->hoff[q], sizeof(uint64_t) * ((size_t)need[q] * nx + 1))) ||
+                      (s = halo_buf(g, g->hep[q], sizeof(float2) * (recv_n[q] + 1)))))
+        return s;
+    }
+    if ((s = comm_after_main(g))) return s;   // (the allocations above are ordered on the handle's stream)
+    NK(ncclGroupStart());
+    for (int q = 0; q < 2; ++q) {
+      if (peer[q] < 0) continue;
+      const uint64_t* so = (const uint64_t*)g->off.p + (q == 0 ? 0 : (size_t)(g->nrows - sr[q]) * nx);
+      NK(ncclSend(so, (size_t)sr[q] * nx + 1, ncclUint64, peer[q], comm, g->comm));
+      if (h[2 * q]) NK(ncclSend((const float2*)g->ep.p + h[2 * q + 1], 2 * h[2 * q], ncclFloat32, peer[q], comm, g->comm));
+      NK(ncclRecv(g->hoff[q].p, (size_t)need[q] * nx + 1, ncclUint64, peer[q], comm, g->comm));
+      if (recv_n[q]) NK(ncclRecv(g->hep[q].p, 2 * recv_n[q], ncclFloat32, peer[q], comm, g->comm));
+    }
+    NK(ncclGroupEnd());
+    for (int q = 0; q < 2; ++q)
+      if (need[q]) {
+        const uint64_t nc = (uint64_t)need[q] * nx;
+        halo_rebase<<<(unsigned)((nc + 256) / 256), 256, 0, g->comm>>>((uint64_t*)g->hoff[q].p, nc, hdr + 5 + 2 * q, 0);
+      }
+    CK(cudaGetLastError());
+  } else {   // HALO_LOOP: the neighbouring handles of this process
+    for (int q = 0; q < 2; ++q) {
+      if (!need[q]) continue;
+      dexel_grid nb = g->link[q];
+      if (!nb) return fail(DEXEL_EINVAL, "loopback slab: no linked neighbour on side " + std::to_string(q));
+      if (nb->nrows < need[q])
+        return fail(DEXEL_EINVAL, "neighbouring slab has " + std::to_string(nb->nrows) + " rows < R = " + std::to_string(R));
+      const int64_t c0 = q == 0 ? (int64_t)(nb->nrows - need[q]) * nx : 0, nc = (int64_t)need[q] * nx;
+      uint64_t ab[2];
+      CK(cudaStreamSynchronize(nb->stream));   // (its contents are final: ops are not re-entrant)
+      CK(cudaMemcpy(&ab[0], (const uint64_t*)nb->off.p + c0, 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&ab[1], (const uint64_t*)nb->off.p + c0 + nc, 8, cudaMemcpyDeviceToHost));
+      recv_n[q] = ab[1] - ab[0];
+      if ((s = halo_buf(g, g->hoff[q], sizeof(uint64_t) * (nc + 1))) ||
+          (s = halo_buf(g, g->hep[q], sizeof(float2) * (recv_n[q] + 1))))
+        return s;
+      if ((s = comm_after_main(g))) return s;
+      CK(cudaMemcpyAsync(g->hoff[q].p, (const uint64_t*)nb->off.p + c0, sizeof(uint64_t) * (nc + 1), cudaMemcpyDefault,
+                         g->comm));
+      if (recv_n[q])
+        CK(cudaMemcpyAsync(g->hep[q].p, (const float2*)nb->ep.p + ab[0], sizeof(float2) * recv_n[q],
+                           cudaMemcpyDefault, g->comm));
+      halo_rebase<<<(unsigned)((nc + 256) / 256), 256, 0, g->comm>>>((uint64_t*)g->hoff[q].p, (uint64_t)nc, nullptr, ab[0]);
+      CK(cudaGetLastError());
+    }
+  }
+  CK(cudaEventRecord(g->ev_halo, g->comm));
+  g->halo_pending = true;
+  for (int q = 0; q < 2; ++q) {
+    g->hrows[q] = need[q];
+    g->hn[q] = recv_n[q];
+  }
+  return DEXEL_OK;
+}
+
+// the handle's stream waits for an exchange still in flight (before any later free or reuse of the
+// halo buffers on that stream)
+void halo_end(dexel_grid g) {
+  if (g->halo_pending) cudaStreamWaitEvent(g->stream, g->ev_halo, 0);
+  g->halo_pending = false;
 }
 
 dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst, bool slices) {
@@ -755,41 +991,24 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   const int Rmax = slices ? 0 : (Ra > Rb ? Ra : Rb);
   const int need_lo = src->d.y0 < Rmax ? src->d.y0 : Rmax;
   const int need_hi = src->d.ny - src->d.y1 < Rmax ? src->d.ny - src->d.y1 : Rmax;
-  if (src->hrows[0] < need_lo || src->hrows[1] < need_hi)
-    return fail(DEXEL_EINVAL, "slab halo too small: need " + std::to_string(need_lo) + " rows below and " +
-                                  std::to_string(need_hi) + " above (dexel_upload_halo)");
-  const int hlo = slices ? 0 : src->hrows[0], hhi = slices ? 0 : src->hrows[1];
-  const int nrows_ext = hlo + src->nrows + hhi;
-  const uint64_t* ext_off = (const uint64_t*)src->off.p;
-  const float* ext_ep = (const float*)src->ep.p;
-  if (hlo || hhi) {
-    const int64_t nx = src->d.nx;
-    const int64_t ncol_ext = (int64_t)nrows_ext * nx;
-    const uint64_t next = src->hn[0] + src->n + src->hn[1];
-    uint64_t* eo = nullptr;
-    float2* ee = nullptr;
-    if ((s = T.get(sizeof(uint64_t) * (ncol_ext + 1), (void**)&eo))) return s;
-    if ((s = T.get(sizeof(float2) * (next + 1), (void**)&ee))) return s;
-    const Buf* parts_off[3] = {&src->hoff[0], &src->off, &src->hoff[1]};
-    const Buf* parts_ep[3] = {&src->hep[0], &src->ep, &src->hep[1]};
-    const int64_t part_cols[3] = {(int64_t)hlo * nx, src->ncol, (int64_t)hhi * nx};
-    const uint64_t part_n[3] = {src->hn[0], src->n, src->hn[1]};
-    int64_t cbase = 0;
-    uint64_t ebase = 0;
-    for (int q = 0; q < 3; ++q) {
-      if (part_cols[q] == 0) continue;
-      rebase_offsets<<<(unsigned)((part_cols[q] + 256) / 256), 256, 0, st>>>(
-          (const uint64_t*)parts_off[q]->p, (uint64_t)part_cols[q], ebase, eo + cbase);
-      if (part_n[q]) CK(cudaMemcpyAsync(ee + ebase, parts_ep[q]->p, sizeof(float2) * part_n[q],
-                                        cudaMemcpyDeviceToDevice, st));
-      cbase += part_cols[q];
-      ebase += part_n[q];
-    }
-    CK(cudaGetLastError());
-    ext_off = eo;
-    ext_ep = (const float*)ee;
+  const int hmode = halo_mode(src);
+  int hlo = 0, hhi = 0;
+  if (hmode != HALO_CALLER) {   // the library exchanges the halo rows itself (NCCL or loopback)
+    if (Rmax > 0 && (s = halo_begin(src, Rmax))) return s;
+    hlo = need_lo;
+    hhi = need_hi;
+  } else {
+    if (src->hrows[0] < need_lo || src->hrows[1] < need_hi)
+      return fail(DEXEL_EINVAL, "slab halo too small: need " + std::to_string(need_lo) + " rows below and " +
+                                    std::to_string(need_hi) + " above (dexel_upload_halo)");
+    hlo = slices ? 0 : src->hrows[0];
+    hhi = slices ? 0 : src->hrows[1];
   }
-  SrcRows rows{ext_off, ext_ep, src->d.nx, nrows_ext, src->d.z_lo, src->d.z_hi};
+  const int nrows_ext = hlo + src->nrows + hhi;
+  SrcRows rows{{(const uint64_t*)src->hoff[0].p, (const uint64_t*)src->off.p, (const uint64_t*)src->hoff[1].p},
+               {(const float*)src->hep[0].p, (const float*)src->ep.p, (const float*)src->hep[1].p},
+               {hlo, src->nrows, hhi},
+               src->d.nx, nrows_ext, src->d.z_lo, src->d.z_hi};
   stats.n_in = src->n;
   // h(kappa, k) tables, one per family radius
   float* htab_a = nullptr;
@@ -922,6 +1141,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   stats.bands = (uint32_t)((src->nrows + band - 1) / band);
   stats.p2_acc = acc;
   uint64_t nout = 0;
+  dst->n = 0;   // (from here on dst is being replaced: an error leaves it empty, run_op)
   if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
   if ((s = scan_counts(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p, &nout))) return s;
   {   // the output endpoints: the current buffer is reused when the size fits (dst != src)
@@ -959,7 +1179,15 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
 // an op that ran out of device memory drops the cached band budget (the next op re-queries)
 dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst, bool slices = false) {
   const dexel_status s = run_op_impl(op, src, r_a, r_b, dst, slices);
+  if (src) halo_end(src);
   if (s == DEXEL_ENOMEM && src) dev_ws(src->d.device).band_budget = 0;
+  // dst is replaced; on any error it is left empty, never partially written (dexel.h).  (src == dst
+  // and NULL handles are rejected before anything is touched and leave both as they were.)
+  if (s != DEXEL_OK && dst && dst != src) {
+    const std::string msg = g_err;
+    set_empty(dst);
+    g_err = msg;
+  }
   return s;
 }
 
@@ -1226,8 +1454,9 @@ namespace {
 dexel_status compose(int op1, int op2, dexel_grid src, float r, dexel_grid dst) {
   if (!src || !dst) return fail(DEXEL_EINVAL, "NULL handle");
   if (src == dst) return fail(DEXEL_EINVAL, "src and dst must be different handles");
-  if (src->d.nranks > 1)
-    return fail(DEXEL_EINVAL, "opening/closing of a y-slab needs the intermediate's halo rows: compose "
+  if (src->d.nranks > 1 && !src->d.nccl_comm)
+    return fail(DEXEL_EINVAL, "opening/closing of a y-slab needs the intermediate's halo rows: give the slabs an "
+                              "NCCL communicator (the intermediate is exchanged like any input), or compose "
                               "dexel_erode/dexel_dilate with a halo exchange in between");
   dexel_desc d = src->d;
   d.stream = (void*)src->stream;
@@ -1405,7 +1634,8 @@ dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offset
   if ((s = check_radius(r, g->d.spacing, &R))) return s;
   CK(cudaSetDevice(g->d.device));
   Temps T(g);
-  SrcRows rows{(const uint64_t*)g->off.p, (const float*)g->ep.p, g->d.nx, g->nrows, g->d.z_lo, g->d.z_hi};
+  SrcRows rows{{nullptr, (const uint64_t*)g->off.p, nullptr}, {nullptr, (const float*)g->ep.p, nullptr},
+               {0, g->nrows, 0}, g->d.nx, g->nrows, g->d.z_lo, g->d.z_hi};
   PieceSlots P;
   uint64_t m = 0;
   // unfiltered pieces (no capsule-domination pruning): bitwise comparable with the oracle's P1
@@ -1462,6 +1692,15 @@ void dexel_destroy(dexel_grid g) {
   }
   dfree(g, g->spare_off);
   dfree(g, g->spare_ep);
+  dfree(g, g->hdr);
+  if (g->comm) {
+    cudaStreamSynchronize(g->comm);
+    cudaStreamDestroy(g->comm);
+  }
+  if (g->ev_main) cudaEventDestroy(g->ev_main);
+  if (g->ev_halo) cudaEventDestroy(g->ev_halo);
+  for (int q = 0; q < 2; ++q)   // unlink from loopback neighbours
+    if (g->link[q] && g->link[q]->link[1 - q] == g) g->link[q]->link[1 - q] = nullptr;
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   if (g->pin) cudaFreeHost(g->pin);
@@ -1503,6 +1742,58 @@ dexel_status dexel_set_timing(int on) {
 dexel_status dexel_last_stats(dexel_grid g, dexel_stats* out) {
   if (!g || !out) return fail(DEXEL_EINVAL, "NULL argument");
   *out = g->stats;
+  return DEXEL_OK;
+}
+
+dexel_status dexel_nccl_unique_id(uint8_t id[128]) {
+  g_err.clear();
+  if (!id) return fail(DEXEL_EINVAL, "NULL argument");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId u;
+  NK(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return DEXEL_OK;
+}
+
+dexel_status dexel_nccl_comm_init(const uint8_t id[128], int nranks, int rank, int device, void** comm) {
+  g_err.clear();
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(DEXEL_EINVAL, "bad communicator arguments");
+  CK(cudaSetDevice(device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t c = nullptr;
+  NK(ncclCommInitRank(&c, nranks, u, rank));
+  *comm = (void*)c;
+  return DEXEL_OK;
+}
+
+dexel_status dexel_nccl_comm_destroy(void* comm) {
+  g_err.clear();
+  if (!comm) return DEXEL_OK;
+  NK(ncclCommDestroy((ncclComm_t)comm));
+  return DEXEL_OK;
+}
+
+dexel_status dexel_link_slabs(dexel_grid* slabs, int n) {
+  g_err.clear();
+  if (!slabs || n < 1) return fail(DEXEL_EINVAL, "bad slab list");
+  for (int q = 0; q < n; ++q) {
+    const dexel_grid g = slabs[q];
+    if (!g) return fail(DEXEL_EINVAL, "NULL slab handle");
+    const dexel_desc& d = g->d;
+    if (d.nranks != n || d.rank != q || d.nccl_comm)
+      return fail(DEXEL_EINVAL, "slab " + std::to_string(q) + " must have rank " + std::to_string(q) + " of nranks " +
+                                    std::to_string(n) + " and no NCCL communicator");
+    const dexel_desc& d0 = slabs[0]->d;
+    if (d.nx != d0.nx || d.ny != d0.ny || d.spacing != d0.spacing || d.z_lo != d0.z_lo || d.z_hi != d0.z_hi)
+      return fail(DEXEL_EINVAL, "slabs must share the grid geometry");
+    if ((q == 0 && d.y0 != 0) || (q > 0 && d.y0 != slabs[q - 1]->d.y1) || (q + 1 == n && d.y1 != d.ny))
+      return fail(DEXEL_EINVAL, "the slabs' rows [y0, y1) must tile [0, ny) in rank order");
+  }
+  for (int q = 0; q < n; ++q) {
+    slabs[q]->link[0] = q > 0 ? slabs[q - 1] : nullptr;
+    slabs[q]->link[1] = q + 1 < n ? slabs[q + 1] : nullptr;
+  }
   return DEXEL_OK;
 }
 

@@ -49,10 +49,15 @@ __global__ void validate_kernel(const uint64_t* __restrict__ off, const float* _
 }
 
 // ------------------------------------------------------------------ pass 1
+// The rows an op reads, in "extended" numbering 0 .. nrows-1: up to three CSR segments stacked
+// along y -- the halo rows below the slab (segment 0: received from rank g-1, DESIGN.md
+// "Multi-GPU"), the slab's own rows (1), the halo rows above it (2).  Each segment is a plain
+// CSR with offsets starting at 0; no copy joins them.
 struct SrcRows {
-  const uint64_t* off;  // CSR offsets of the source rows (nrows*nx + 1)
-  const float* ep;      // flat endpoints
-  int nx, nrows;
+  const uint64_t* off[3];   // CSR offsets of each segment's rows (rows[s]*nx + 1)
+  const float* ep[3];       // flat endpoints of each segment
+  int rows[3];
+  int nx, nrows;            // nrows = rows[0] + rows[1] + rows[2]
   float zlo, zhi;
 };
 
@@ -60,28 +65,34 @@ struct SrcRows {
 // [zlo,zhi] (complement-on-load): [zlo,a0],[b0,a1],...,[b_{n-1},zhi]
 // with zero-length end pieces dropped.  Even virtual index = start, odd = end.
 struct ColCursor {
-  uint64_t base;
+  const float* p;   // the column's first endpoint
   uint32_t n, v, vend;
 };
 
 __device__ __forceinline__ float col_value(const SrcRows& s, const ColCursor& c, uint32_t v, int complement) {
-  if (!complement) return __ldg(s.ep + 2 * c.base + v);
+  if (!complement) return __ldg(c.p + v);
   if (v == 0) return s.zlo;
   if (v == 2 * c.n + 1) return s.zhi;
-  return __ldg(s.ep + 2 * c.base + v - 1);
+  return __ldg(c.p + v - 1);
 }
 
+__device__ __forceinline__ void col_close(ColCursor& c) { c.p = nullptr; c.n = 0; c.v = 0; c.vend = 0; }
+
 __device__ __forceinline__ void col_open(const SrcRows& s, int i, int j, int complement, ColCursor& c) {
-  if (i < 0 || i >= s.nx || j < 0 || j >= s.nrows) { c.base = 0; c.n = 0; c.v = 0; c.vend = 0; return; }
+  if (i < 0 || i >= s.nx || j < 0 || j >= s.nrows) { col_close(c); return; }
+  int seg = 0;
+  if (j >= s.rows[0]) { j -= s.rows[0]; seg = 1; }
+  if (seg == 1 && j >= s.rows[1]) { j -= s.rows[1]; seg = 2; }
+  const uint64_t* off = s.off[seg];
   size_t col = (size_t)j * s.nx + i;
-  uint64_t a = __ldg(s.off + col), b = __ldg(s.off + col + 1);
-  c.base = a;
+  uint64_t a = __ldg(off + col), b = __ldg(off + col + 1);
+  c.p = s.ep[seg] + 2 * a;
   c.n = (uint32_t)(b - a);
   if (!complement) { c.v = 0; c.vend = 2 * c.n; return; }
   c.v = 0;
   c.vend = 2 * c.n + 2;
-  if (c.n > 0 && __ldg(s.ep + 2 * a) <= s.zlo) c.v = 2;                 // S touches z_lo
-  if (c.n > 0 && __ldg(s.ep + 2 * (b - 1) + 1) >= s.zhi) c.vend = 2 * c.n;  // S touches z_hi
+  if (c.n > 0 && __ldg(c.p) <= s.zlo) c.v = 2;                              // S touches z_lo
+  if (c.n > 0 && __ldg(c.p + 2 * (c.n - 1) + 1) >= s.zhi) c.vend = 2 * c.n;  // S touches z_hi
   if (s.zlo >= s.zhi) c.vend = c.v;
 }
 
@@ -169,8 +180,14 @@ constexpr int P1_RING = 8;       // pending closed pieces per lane
 // of the synthetic configs go.  The next piece n lies above the pending one p, so the two tests
 // reduce to  n dominates p: kn <= kp and lo_n - lo_p <= H[kn] - H[kp];  p dominates n:
 // kp <= kn and hi_n - hi_p <= H[kp] - H[kn]  (H = h(., 0), fp32).  Both sides are differences
-// of nearby values (error ~2^-24 of the result), and a piece is only dropped with a relative
-// margin of 1e-6, so rounding can keep a dominated piece but never drop a needed one.
+// of nearby values.  A piece is only dropped with a margin of 1e-6 (1 + |D|) + 16 r 2^-24
+// (prune[R+1]): the H table rounds each h(., 0) <= r by <= ulp(r)/2 and the two differences
+// round by <= ulp(r)/2 each, so a dropped piece's capsule lies inside the dominating one's in
+// exact arithmetic with a slack of >= ulp(r) at level 0 (the margin 16 r 2^-24 is >= 8 ulp(r);
+// the threshold's own fp32 roundings and that of z - phi cost at most 3.5 ulp(r)) -- and the slack only grows with the
+// level k -- which also covers the fp32 rounding of the level-k grown endpoints
+// fl32(lo - fl32(h)): pruning leaves the output bitwise unchanged (GPU test against
+// DEXEL_NO_PRUNE=1).  Rounding can keep a dominated piece, never drop a needed one.
 // predicated store of one piece (8-byte z pair + kappa byte) without a branch
 __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo, float hi, int k, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v2.f32 [%0], {%2, %3};\n\t"
@@ -178,14 +195,29 @@ __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo,
                :: "l"(zp), "l"(kp), "f"(lo), "f"(hi), "r"(k), "r"((int)pred));
 }
 
-__device__ __forceinline__ bool dom_margin(float lhs, float rhs) {
-  return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs));
+__device__ __forceinline__ bool dom_margin(float lhs, float rhs, float mabs) {
+  return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs)) - mabs;
+}
+
+// capsule-domination thresholds of every (pending kappa, new kappa) pair (see p1_kernel)
+__device__ __forceinline__ void p1_thr_init(float2* thr, const float* __restrict__ prune, int R) {
+  const float mabs = prune[R + 1];   // absolute part of the margin (16 r 2^-24, see above)
+  for (int t = threadIdx.x; t < 18 * 32; t += blockDim.x) {
+    const int kp = t >> 5, kn = t & 31;
+    float2 v = make_float2(-INFINITY, -INFINITY);
+    if (kp <= R && kn <= R) {
+      const float D = prune[kp] - prune[kn];                // H[kp] - H[kn]
+      if (kp <= kn) v.x = D - 1e-6f * (1.0f + fabsf(D)) - mabs;    // drop new:     hi_n - hi_p <= x
+      if (kn <= kp) v.y = -D - 1e-6f * (1.0f + fabsf(D)) - mabs;   // drop pending: lo_n - lo_p <= y
+    }
+    thr[t] = v;
+  }
 }
 
 // SKIP (host: R >= 8): steps where no lane's kappa changes skip the filter / emission half
 template <int NW, bool RING, bool SKIP = true>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, int complement, int row0,
-                                                            int nrows_out, PieceSlots P, int64_t nlist,
+                                                            int jr0, int nrows_out, PieceSlots P, int64_t nlist,
                                                             const float* __restrict__ prune) {
   __shared__ uint32_t stage_all[P1_WARPS][P1_STAGE];
   __shared__ float h0[256];
@@ -196,20 +228,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   __shared__ float2 thr[(NW == 2 && !RING) ? 18 * 32 : 1];
   __shared__ float2 ring_z[P1_WARPS][RING ? P1_RING : 1][32];   // closed pieces awaiting the filter / store
   __shared__ uint8_t ring_k[P1_WARPS][RING ? P1_RING : 1][32];
+  const float mabs = prune ? prune[R + 1] : 0.f;   // absolute part of the domination margin
   if (prune) {
     for (int t = threadIdx.x; t <= R; t += blockDim.x) h0[t] = prune[t];
-    if constexpr (NW == 2 && !RING) {
-      for (int t = threadIdx.x; t < 18 * 32; t += blockDim.x) {
-        const int kp = t >> 5, kn = t & 31;
-        float2 v = make_float2(-INFINITY, -INFINITY);
-        if (kp <= R && kn <= R) {
-          const float D = prune[kp] - prune[kn];                // H[kp] - H[kn]
-          if (kp <= kn) v.x = D - 1e-6f * (1.0f + fabsf(D));    // drop new:     hi_n - hi_p <= x
-          if (kn <= kp) v.y = -D - 1e-6f * (1.0f + fabsf(D));   // drop pending: lo_n - lo_p <= y
-        }
-        thr[t] = v;
-      }
-    }
+    if constexpr (NW == 2 && !RING) p1_thr_init(thr, prune, R);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -218,7 +240,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   const bool list_mode = nlist >= 0;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= (list_mode ? nlist : (int64_t)nrows_out * ntiles)) return;  // warp-uniform
-  const int64_t tl = list_mode ? (int64_t)P.tile_list[gw] : gw;
+  // main mode: slot rows jr0 .. jr0 + nrows_out - 1 of the band; list mode: the listed tiles
+  const int64_t tl = list_mode ? (int64_t)P.tile_list[gw] : gw + (int64_t)jr0 * ntiles;
   const int jr = (int)(tl / ntiles), tile = (int)(tl % ntiles);
   const int j = row0 + jr;
   const int i0 = tile * 32;
@@ -231,7 +254,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
   for (int q = 0; q < NW; ++q) {
     const int w = lane + 32 * q;
     if (w < W) col_open(src, i0 - R + w, j, complement, cur[q]);
-    else { cur[q].base = 0; cur[q].n = 0; cur[q].v = 0; cur[q].vend = 0; }
+    else col_close(cur[q]);
     const uint32_t nv = cur[q].vend - cur[q].v + 1;    // + a KEY_NONE sentinel
     uint32_t incl = nv;
 #pragma unroll
@@ -330,8 +353,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
         plo = v.x; phi = v.y; pk = kv;
       } else {
         const float D = h0[pk] - h0[kv];                    // H[kp] - H[kn]
-        if (pk <= kv && dom_margin(v.y - phi, D)) continue; // the pending piece covers the new one
-        if (!(kv <= pk && dom_margin(v.x - plo, -D))) put(plo, phi, pk);
+        if (pk <= kv && dom_margin(v.y - phi, D, mabs)) continue; // the pending piece covers the new one
+        if (!(kv <= pk && dom_margin(v.x - plo, -D, mabs))) put(plo, phi, pk);
         plo = v.x; phi = v.y; pk = kv;
       }
     }
@@ -403,8 +426,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
           drop_pend = zstart - plo <= th.y;
         } else {
           const float D = hpk - h0[kap & 255];                  // H[kp] - H[kn] (garbage when unused)
-          drop_new = hp && pk <= kap && dom_margin(z - phi, D);
-          drop_pend = kap <= pk && dom_margin(zstart - plo, -D);
+          drop_new = hp && pk <= kap && dom_margin(z - phi, D, mabs);
+          drop_pend = kap <= pk && dom_margin(zstart - plo, -D, mabs);
           hpk = (closed && !drop_new) ? h0[kap & 255] : hpk;
         }
         // the pending piece is stored (unless the new one dominates it) before it is replaced
@@ -470,20 +493,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_kernel(SrcRows src, int R, i
 // of each family is therefore the one its own sweep produces, and so are the filtered pieces.
 // The event half of a sweep step (REDUX, ballots, key advance) and the key staging run once
 // for both families.  Main pass only (overflow columns are redone per family in list mode).
-
-// capsule-domination thresholds of every (pending kappa, new kappa) pair (see p1_kernel)
-__device__ __forceinline__ void p1_thr_init(float2* thr, const float* __restrict__ prune, int R) {
-  for (int t = threadIdx.x; t < 18 * 32; t += blockDim.x) {
-    const int kp = t >> 5, kn = t & 31;
-    float2 v = make_float2(-INFINITY, -INFINITY);
-    if (kp <= R && kn <= R) {
-      const float D = prune[kp] - prune[kn];                // H[kp] - H[kn]
-      if (kp <= kn) v.x = D - 1e-6f * (1.0f + fabsf(D));    // drop new:     hi_n - hi_p <= x
-      if (kn <= kp) v.y = -D - 1e-6f * (1.0f + fabsf(D));   // drop pending: lo_n - lo_p <= y
-    }
-    thr[t] = v;
-  }
-}
 
 // one family's output state in the dual sweep
 struct P1Fam {
@@ -562,7 +571,7 @@ __device__ __forceinline__ void p1_fam_finish(P1Fam& F, PieceSlots& P, int64_t c
 }
 
 template <bool SKIP>
-__global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int R, int row0, int nrows_out,
+__global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int R, int row0, int jr0, int nrows_out,
                                                                  PieceSlots PS, PieceSlots PC,
                                                                  const float* __restrict__ prune_s,
                                                                  const float* __restrict__ prune_c) {
@@ -576,7 +585,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
   const int ntiles = (src.nx + 31) >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= (int64_t)nrows_out * ntiles) return;  // warp-uniform
-  const int jr = (int)(gw / ntiles), tile = (int)(gw % ntiles);
+  const int jr = jr0 + (int)(gw / ntiles), tile = (int)(gw % ntiles);
   const int j = row0 + jr;
   const int i0 = tile * 32;
   const int W = 32 + 2 * R;
@@ -592,7 +601,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1_dual_kernel(SrcRows src, int
     const int gi = i0 - R + w;
     G[q] = __ballot_sync(FULL, w < W && gi >= 0 && gi < src.nx);   // in-grid window columns
     if (w < W) col_open(src, gi, j, 0, cur[q]);
-    else { cur[q].base = 0; cur[q].n = 0; cur[q].v = 0; cur[q].vend = 0; }
+    else col_close(cur[q]);
     const uint32_t nv = cur[q].vend - cur[q].v + 1;
     uint32_t incl = nv;
 #pragma unroll

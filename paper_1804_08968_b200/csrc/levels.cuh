@@ -36,7 +36,8 @@
 // counts cnt[(row*(R+1) + k)*nx + i] (u16).  For a fixed (row, k, t) the nx columns of a
 // row are contiguous, so a warp of 32 consecutive columns writes and (in pass 2) reads
 // 256 contiguous bytes.  A list longer than cap raises a flag: the column is listed and
-// an overflow pass rewrites all its lists into an arena of 255-entry lists and flags their
+// an overflow pass rewrites all its lists into an arena of m-entry lists (m = the most pieces of
+// any listed column) and flags their
 // counts (LV_IN_ARENA: a column can overflow mid-sweep and end with every count <= cap
 // after pops, so the flag, not the count, tells pass 2 where a list is); if too many
 // columns overflow the host reruns the band with a larger cap.
@@ -48,19 +49,23 @@
 
 namespace dexel {
 
-constexpr int LV_OVF_CAP = 255;   // list capacity in the overflow arena
+constexpr int LV_SLOT_MAX = 255;    // largest slot capacity the host grows to (then: the arena)
+constexpr int LV_CNT_MAX = 0x7fff;  // longest list a u16 count (bit 15 = arena flag) can describe
 constexpr uint16_t LV_IN_ARENA = 0x8000;   // count flag: the column's lists live in the overflow arena
 
 struct LevelSlots {
-  uint16_t* cnt;     // [nrows][R+1][nx]  list lengths (<= 255); LV_IN_ARENA set: the list is in the arena
+  uint16_t* cnt;     // [nrows][R+1][nx]  list lengths (<= LV_CNT_MAX); LV_IN_ARENA set: the list is in the arena
   float2* z;         // [nrows][cap+1][R+2][nx]  (unclipped; slot 0 dummy; level R+1 of the last slot = spill cell)
   int R, cap, nx, nrows;
   int ry;            // row offsets pass 2 reads: |dy| <= ry (R; 0 for slices, 2D offsets of each row)
   int row0;          // row (in the op's extended-row numbering) of slot row 0
   // columns with a list longer than cap keep all their lists in the overflow arena:
-  // list k of overflow slot q at ovf_z[(q*(R+1) + k)*(LV_OVF_CAP+1) + t], t = 1..255 (0 dummy)
+  // list k of overflow slot q at ovf_z[(q*(R+1) + k)*(ovf_cap+1) + t], t = 1..ovf_cap (0 dummy);
+  // ovf_cap = the most pieces of any listed column (a level list never holds more components
+  // than the column has pieces: each push starts with one)
   int32_t* ovf_idx;  // [nrows*nx] overflow slot of a column (valid only where some count > cap)
   float2* ovf_z;
+  int ovf_cap;
 };
 
 __host__ __device__ __forceinline__ size_t slot_cnt_index(const LevelSlots& L, int row, int k, int i) {
@@ -75,7 +80,7 @@ __host__ __device__ __forceinline__ size_t slot_z_index(const LevelSlots& L, int
 }
 
 __host__ __device__ __forceinline__ size_t ovf_z_index(const LevelSlots& L, int q, int k, int t) {
-  return ((size_t)q * (L.R + 1) + k) * (LV_OVF_CAP + 1) + t;
+  return ((size_t)q * (L.R + 1) + k) * (size_t)(L.ovf_cap + 1) + t;
 }
 
 struct LvArgs {
@@ -84,7 +89,7 @@ struct LvArgs {
   const float* h;          // [(R+1)^2] fl32(sqrt(r^2 - (kappa^2 + k^2) s^2)), -1 where negative
   float zlo, zhi;
   LevelSlots L;
-  unsigned* flags;         // [0] longest list seen, [1] overflow columns
+  unsigned* flags;         // [0] longest list seen, [1] overflow columns, [2] most pieces of one
   unsigned long long* nlev;  // total level intervals (statistics)
   unsigned long long* dbg; // diagnostics or nullptr: [0] sum of per-warp max piece counts, [1] warps
   uint32_t* ovf_list;      // main pass: columns with a list longer than cap
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   float2* Zd = q < 0 ? A.L.z + slot_z_index(A.L, row, k0, 0, i) : A.L.ovf_z + ovf_z_index(A.L, q, k0, 0);
   const uint32_t nx = (uint32_t)A.L.nx;
   const uint32_t ostep = q < 0 ? (uint32_t)(R + 2) * nx : 1u;           // one slot
-  const uint32_t olev = q < 0 ? nx : (uint32_t)(LV_OVF_CAP + 1);        // one level
-  const uint32_t ncap = q < 0 ? (uint32_t)A.L.cap : (uint32_t)LV_OVF_CAP;
+  const uint32_t olev = q < 0 ? nx : (uint32_t)(A.L.ovf_cap + 1);      // one level
+  const uint32_t ncap = q < 0 ? (uint32_t)A.L.cap : (uint32_t)A.L.ovf_cap;
   // the spill cell: level R+1 of the last slot (main pass), the last arena entry (overflow pass)
   const uint32_t olim = q < 0 ? ncap * ostep + (uint32_t)(R + 1 - k0) * nx : (uint32_t)(R + 1 - k0) * olev - 1u;
   float cs[LMAX], ce[LMAX], pce[LMAX];
@@ -260,7 +265,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     st_pred_f2(Zd + min(o[k], olim), cs[k], ce[k], top);
     const uint32_t nk_ = top ? (o[k] - (uint32_t)k * olev) / ostep : 0u;   // slots 1..n
     if (live && k0 + k <= R) {
-      A.L.cnt[slot_cnt_index(A.L, row, k0 + k, i)] = (uint16_t)(min(nk_, 255u) | (q < 0 ? 0u : LV_IN_ARENA));
+      A.L.cnt[slot_cnt_index(A.L, row, k0 + k, i)] =
+          (uint16_t)(min(nk_, (uint32_t)LV_CNT_MAX) | (q < 0 ? 0u : LV_IN_ARENA));
       tot += nk_;
       mx = max(mx, nk_);
     }
@@ -269,7 +275,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
   if (live && mx > (unsigned)A.L.cap) {
     atomicMax(A.flags, mx);
-    if (q < 0) {   // hand the column to the overflow pass
+    if (q < 0) {   // hand the column to the overflow pass (its arena lists hold up to m pieces)
+      atomicMax(A.flags + 2, (unsigned)m);
       const unsigned slot = atomicAdd(A.flags + 1, 1u);
       if (slot < A.ovf_list_cap) {
         A.ovf_list[slot] = (uint32_t)c;

@@ -143,7 +143,7 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
   // loaded; returns the list length
   auto open = [&](int t, int cw, const float2*& lb, int64_t& st, P2Batch& X) -> int {
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-    const int nb = cw & 0xff;
+    const int nb = cw & LV_CNT_MAX;
     if (!(cw & LV_IN_ARENA)) {
       lb = L.z + slot_z_index(L, jl, k, 1, i);
       st = (int64_t)(L.R + 2) * L.nx;   // one slot
@@ -159,7 +159,7 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
   int64_t st = 0;
   P2Batch X;
   X.n = 0;
-  if (cw & 0xff) n = open(0, cw, lb, st, X);
+  if (cw & LV_CNT_MAX) n = open(0, cw, lb, st, X);
   for (int t = 0; t < nt; ++t) {
     const int nc = n;
     const float2* lbc = lb;
@@ -167,7 +167,7 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
     const P2Batch Xc = X;
     cw = cwn;
     cwn = count(t + 2);
-    n = (cw & 0xff) ? open(t + 1, cw, lb, st, X) : 0;
+    n = (cw & LV_CNT_MAX) ? open(t + 1, cw, lb, st, X) : 0;
     if (nc) acc_insert_list<T>(A, Xc, lbc, nc, stc, scratch, zlo, zhi, cap, need);
   }
 }

@@ -1,16 +1,22 @@
-"""Multi-GPU y-slabs: one process per GPU, halo rows exchanged with torch.distributed.
+"""Multi-GPU y-slabs: one process per GPU, halo rows exchanged inside the library.
 
 The path shards along y ("the 2D dilations can be
 performed completely independently in every slice").  Rank g owns rows
 [y0, y1).  Pass 1 runs along x and is row-local; pass 2 runs along y and reads
-R = floor(r/s) rows beyond each slab boundary.  Those rows are the only
-data-path exchange: every op, each rank packs its first and last R owned rows
-(dexel_download_rows, device buffers), sends them to ranks g-1 / g+1 with
-point-to-point send/recv (NCCL over NVLink on GPUs, gloo on CPU tests) and
-attaches what it receives as halos (dexel_upload_halo).  The exchange is two
-phase because rows are ragged: interval counts first, then offsets and
-endpoints.  Input halos (not pass-1 output) are exchanged: they are ~n_mid/n_in
-times smaller, and one exchange serves both families of a shell.
+R = floor(r/s) rows of input beyond each slab boundary -- the only data-path
+exchange.  Transports (include/dexel.h "Multi-GPU"):
+
+  "nccl"      the library's own NCCL send/recv inside every (collective) op,
+              overlapped with pass 1 of the slab's interior rows.  The
+              communicator is bootstrapped here: rank 0 draws the NCCL unique
+              id, torch.distributed broadcasts its 128 bytes, every rank calls
+              dexel_nccl_comm_init.
+  "loopback"  several slab handles in one process (one GPU in tests): the
+              library copies the halo rows from the linked neighbour handles
+              (dexel_link_slabs) -- the same halo layout and pass-1 split.
+  "caller"    the caller moves the rows: dexel_download_rows packs them, a
+              torch.distributed point-to-point exchange (gloo in the CPU tests)
+              moves them, dexel_upload_halo attaches them.
 
 Host-side helpers here hold no method arithmetic; they are plumbing.
 """
@@ -97,23 +103,57 @@ def halo_exchange(send_lo, send_hi, rank: int, world: int, nrows_lo: int, nrows_
     return halo_lo, halo_hi
 
 
-class Slab:
-    """One rank's slab of a dexel grid on its GPU (src handle with halos + dst handle)."""
+def broadcast_unique_id(rank: int, device: Optional[int] = None, group=None) -> bytes:
+    """Rank 0 draws the 128-byte NCCL unique id (dexel_nccl_unique_id); torch.distributed
+    broadcasts it (a CUDA tensor under the nccl backend, a CPU tensor under gloo)."""
+    import torch
+    import torch.distributed as dist
 
-    def __init__(self, host, rank: int, world: int, device: int, stream: Optional[int] = None):
+    import paper_1804_08968_b200 as dx
+    on_gpu = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", device or 0) if on_gpu else torch.device("cpu")
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(dx.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.cpu().tolist())
+
+
+def nccl_bootstrap(rank: int, world: int, device: int, group=None) -> int:
+    """ncclComm_t for the library: the broadcast unique id, then dexel_nccl_comm_init on every
+    rank (collective)."""
+    import paper_1804_08968_b200 as dx
+    return dx.nccl_comm_init(broadcast_unique_id(rank, device, group), world, rank, device)
+
+
+class Slab:
+    """One rank's slab of a dexel grid on its GPU (src handle + dst handle)."""
+
+    def __init__(self, host, rank: int, world: int, device: int, stream: Optional[int] = None,
+                 transport: str = "caller", comm: Optional[int] = None):
         import paper_1804_08968_b200 as dx
+        if transport not in ("nccl", "loopback", "caller"):
+            raise ValueError(f"unknown transport {transport!r}")
+        if transport == "nccl" and world > 1 and not comm:
+            raise ValueError("transport 'nccl' needs a communicator (nccl_bootstrap)")
         self.dx = dx
+        self.transport = transport
         self.rank, self.world, self.nx, self.ny = rank, world, host.nx, host.ny
         self.y0, self.y1 = slab_bounds(host.ny, world, rank)
         self.src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi, getattr(host, "z_ref", 0.0),
-                           getattr(host, "spacing", 1.0), device, stream, self.y0, self.y1, rank, world)
+                           getattr(host, "spacing", 1.0), device, stream, self.y0, self.y1, rank, world,
+                           comm if transport == "nccl" else None)
         off, ep = csr_rows(host.off, host.ep, host.nx, self.y0, self.y1 - self.y0)
         self.src.upload(off, ep)
         self.dst = dx.Grid.like(self.src)
         self.halo_rows = -1
 
     def refresh_halos(self, R: int, group=None):
-        """Exchange R boundary rows with the neighbours over torch.distributed (device buffers)."""
+        """Caller-managed transport only: exchange R boundary rows with the neighbours over
+        torch.distributed (device buffers) and attach them.  (NCCL / loopback slabs exchange
+        inside every op.)"""
+        if self.transport != "caller":
+            return
         nrows = self.y1 - self.y0
         send = min(R, nrows)
         lo = self.src.download_rows(0, send, device=True) if self.rank > 0 else None
@@ -130,10 +170,35 @@ class Slab:
 
     def op(self, op: str, r: float, r2: Optional[float] = None):
         dx = self.dx
-        if op in ("dilate", "erode", "dilate_slices", "erode_slices"):
+        if op in ("dilate", "erode", "dilate_slices", "erode_slices", "open", "close"):
             getattr(dx, "dexel_" + op)(self.src, r, self.dst)
         elif op in ("shell", "shell_slices"):
             getattr(dx, "dexel_" + op)(self.src, r, r if r2 is None else r2, self.dst)
         else:
             raise ValueError(f"unknown op {op!r}")
         return self.dst
+
+    def close(self):
+        self.src.close()
+        self.dst.close()
+
+
+def loopback_slabs(host, world: int, device: int = 0, stream: Optional[int] = None):
+    """`world` slab handles of one grid in this process, linked for in-library halo copies
+    (dexel_link_slabs); their ops need no exchange by the caller."""
+    import paper_1804_08968_b200 as dx
+    slabs = [Slab(host, g, world, device, stream, transport="loopback") for g in range(world)]
+    if world > 1:
+        dx.link_slabs([s.src for s in slabs])
+    return slabs
+
+
+def concat_slabs(parts):
+    """Concatenate per-slab CSRs (off, ep) in rank order into one global CSR (host numpy)."""
+    base, offs, eps = 0, [np.zeros(1, np.uint64)], []
+    for o, e in parts:
+        o = np.asarray(o, dtype=np.uint64)
+        offs.append(o[1:] + np.uint64(base))
+        base += int(o[-1])
+        eps.append(np.asarray(e, dtype=np.float32))
+    return np.concatenate(offs), (np.concatenate(eps) if eps else np.zeros(0, np.float32))

@@ -698,3 +698,77 @@ def test_trim_workspace_keeps_results(dx):
         dx.trim_workspace(-1)
     src.close()
     dst.close()
+
+
+# ---------------------------------------------------------------- parameter space (round 2)
+@pytest.mark.parametrize("r", [65.0, 80.5, 128.0, 255.0])
+def test_ops_large_radius(dx, r):
+    """Ops at R = floor(r/s) in (64, 255]: every pass-1 mask width (NW = 5, 9, 17) and level
+    chunking, against the oracle on every column."""
+    host = G.random_grid(37, 29, 4, -300.0, 300.0, int(r) + 5)
+    for op in ("dilate", "erode", "shell"):
+        off, ep, _ = run_gpu(dx, host, op, r, r if op == "shell" else None)
+        check(off, ep, run_oracle(host, op, r), what=f"{op} r={r}")
+
+
+@pytest.mark.parametrize("s", [0.5, 1.7, 0.3])
+def test_ops_spacing(dx, s):
+    """Lateral spacing s != 1 (R = floor(r/s), weights r^2 - (kappa^2 + dy^2) s^2)."""
+    for seed in range(3):
+        host = G.random_grid(31, 23, 4, -12.0, 12.0, 300 + seed, quantum=0.25 if seed == 1 else None)
+        host.spacing = s
+        for r in (0.2, 1.0, 2.6, 5.0):
+            for op in ("dilate", "erode", "shell"):
+                off, ep, _ = run_gpu(dx, host, op, r, r * 0.8 if op == "shell" else None)
+                check(off, ep, run_oracle(host, op, r, r * 0.8 if op == "shell" else None),
+                      what=f"spacing {s} {op} r={r}")
+
+
+@pytest.mark.parametrize("op", ["dilate", "erode", "shell"])
+def test_many_layer_column(dx, op):
+    """300 thin layers in a column (level lists and unions far beyond every default capacity,
+    level lists beyond the old 255-interval arena): the op succeeds and matches the oracle."""
+    col = [(float(t) * 0.5 - 80.0, float(t) * 0.5 - 79.8) for t in range(300)]
+    cols = [col if (i + 2 * j) % 3 == 0 else (col[::3] if i % 2 else []) for j in range(5) for i in range(6)]
+    host = _grid(6, 5, cols, -81.0, 81.0)
+    for r in (0.05, 0.4, 1.3):
+        off, ep, _ = run_gpu(dx, host, op, r)
+        check(off, ep, run_oracle(host, op, r), what=f"300 layers {op} r={r}")
+
+
+def test_caller_stream(dx):
+    """A handle on a caller-supplied stream (torch side stream): ops run on it, results match the
+    oracle, and work queued on the stream before the op is ordered before it."""
+    import torch
+    host = G.config("C2")
+    st = torch.cuda.Stream()
+    src = dx.Grid(host.nx, host.ny, host.z_lo, host.z_hi, host.z_ref, 1.0, 0, st.cuda_stream)
+    with torch.cuda.stream(st):
+        off_d = torch.from_numpy(host.off.astype(np.int64)).cuda()
+        ep_d = torch.from_numpy(host.ep).cuda()
+    src.upload(off_d, ep_d)
+    dst = dx.Grid.like(src)
+    assert dst.desc.stream == st.cuda_stream
+    dx.dexel_shell(src, 4.0, 4.0, dst)
+    off, ep = dst.download(device=True)
+    st.synchronize()
+    check(off.cpu().numpy().astype(np.uint64), ep.cpu().numpy(), run_oracle(host, "shell", 4.0), what="caller stream")
+    src.close()
+    dst.close()
+
+
+def test_error_leaves_dst_empty(dx):
+    """An op that fails after dst was already written leaves dst empty (dexel.h), and dst is
+    usable afterwards."""
+    host = G.config("C1")
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    dx.dexel_dilate(src, 3.0, dst)
+    assert dst.size() > 0
+    with pytest.raises(dx.DexelError):
+        dx.dexel_dilate(src, float("inf"), dst)
+    assert dst.size() == 0
+    off, _ = dst.download()
+    assert not off.any()
+    dx.dexel_dilate(src, 3.0, dst)
+    check(*dst.download(), run_oracle(host, "dilate", 3.0), what="after error")

@@ -415,3 +415,101 @@ def test_generator_c1_deterministic():
     assert np.array_equal(a.off, b.off) and np.array_equal(a.ep, b.ep)
     # every non-empty column of C1 is one interval (sphere chords overlap the box z-range)
     assert G.stats(a)["max_per_col"] == 1
+
+
+# ---------------------------------------------------------------- lateral spacing s != 1
+def _with_spacing(g, s):
+    g.spacing = float(s)
+    return g
+
+
+@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("s,r", [(0.5, 1.3), (0.5, 2.6), (1.7, 3.5), (2.0, 4.0), (0.25, 1.1)])
+def test_box_dilation_closed_form_spacing(method, s, r):
+    """P5 with lateral spacing s: the nearest footprint column lies at lateral distance
+    d = s * sqrt(di^2 + dj^2); the column dilates to [z0 - h, z1 + h], h = sqrt(r^2 - d^2)."""
+    box = (6, 9, 5, 11, -3.0, 4.5)
+    g = _with_spacing(_box_grid(18, 17, box), s)
+    d = O.dilate(g, r, method)
+    i0, i1, j0, j1, z0, z1 = box
+    for c in range(g.ncol):
+        i, j = c % g.nx, c // g.nx
+        di = max(i0 - i, 0, i - i1)
+        dj = max(j0 - j, 0, j - j1)
+        d2 = float(di * di + dj * dj) * s * s
+        got = d.column(c).tolist()
+        if d2 > r * r:
+            assert got == [], (i, j, got)
+        else:
+            h = math.sqrt(r * r - d2)
+            assert len(got) == 1
+            assert abs(got[0][0] - max(z0 - h, g.z_lo)) < 1e-12 and abs(got[0][1] - min(z1 + h, g.z_hi)) < 1e-12
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("method", METHODS)
+def test_endpoint_distance_bruteforce_spacing(seed, method):
+    """P3 with lateral spacing s != 1: every non-clip output endpoint lies at distance exactly r
+    from the lattice solid, interval midpoints within r, gap midpoints beyond r."""
+    g, r = random_case(seed + 2000, maxn=5, maxk=2, rvals=(1.0, 1.5, 2.7))
+    s = (0.6, 1.4, 0.35)[seed % 3]
+    _with_spacing(g, s)
+    S = grid_cols(g)
+    d = O.dilate(g, r, method)
+    for c in range(g.ncol):
+        i, j = c % g.nx, c // g.nx
+        iv = d.column(c)
+        for lo, hi in iv:
+            for e in (lo, hi):
+                if e in (g.z_lo, g.z_hi):
+                    continue
+                assert abs(dist_to_solid(S, g.nx, g.ny, i, j, e, s) - r) <= 1e-9 * max(1.0, r)
+            assert dist_to_solid(S, g.nx, g.ny, i, j, 0.5 * (lo + hi), s) <= r + 1e-12
+        pts = [g.z_lo] + [x for ab in iv for x in ab] + [g.z_hi]
+        for a, b in zip(pts[0::2], pts[1::2]):
+            if b - a > 1e-9:
+                assert dist_to_solid(S, g.nx, g.ny, i, j, 0.5 * (a + b), s) > r
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_brute_equals_separable_spacing(seed):
+    """P2 (App. A1) with s != 1: O1 and O2 agree bitwise."""
+    g, r = random_case(seed + 3000)
+    _with_spacing(g, (0.5, 1.5, 0.8, 2.25)[seed % 4])
+    for op in ("dilate", "erode"):
+        a = getattr(O, op)(g, r, "brute")
+        b = getattr(O, op)(g, r, "sep")
+        assert np.array_equal(a.off, b.off) and np.array_equal(a.z, b.z), op
+
+
+# ---------------------------------------------------------------- large radii R in (64, 255]
+@pytest.mark.parametrize("r", [70.0, 100.5, 255.0])
+def test_brute_equals_separable_large_radius(r):
+    """P2 at radii whose level count R + 1 exceeds 65 (u8 kappa up to 255)."""
+    g = G.random_grid(9, 7, 3, -300.0, 300.0, int(r))
+    for op in ("dilate", "erode"):
+        a = getattr(O, op)(g, r, "brute")
+        b = getattr(O, op)(g, r, "sep")
+        assert np.array_equal(a.off, b.off) and np.array_equal(a.z, b.z), op
+
+
+# ---------------------------------------------------------------- the sampled-column path
+@pytest.mark.parametrize("seed", range(30))
+def test_sampled_columns_equal_full_run(seed):
+    """oracle_run on a list of columns (the path every C3-C5 parity test and the cpu baseline
+    use) gives bitwise the full run's result for those columns, for every op."""
+    rs = np.random.default_rng(4000 + seed)
+    g = G.random_grid(int(rs.integers(1, 30)), int(rs.integers(1, 30)), 4, -10.0, 10.0, seed,
+                      quantum=0.5 if seed % 2 else None)
+    r = float(rs.choice([0.0, 0.7, 1.0, 2.5, 4.0, 7.0]))
+    cols = np.unique(rs.integers(0, g.ncol, max(1, g.ncol // 3))).astype(np.int64)
+    for op in ("dilate", "erode", "shell", "pass1"):
+        if op == "shell":
+            full, part = O.shell(g, r, r * 0.5), O.shell(g, r, r * 0.5, cols=cols)
+        else:
+            full, part = getattr(O, op)(g, r), getattr(O, op)(g, r, cols=cols)
+        want = [full.column(int(c)) for c in cols]
+        got = [part.column(t) for t in range(len(cols))]
+        assert all(np.array_equal(a, b) for a, b in zip(want, got)), (op, r)
+        if op == "pass1":
+            assert all(np.array_equal(full.kappa(int(c)), part.kappa(t)) for t, c in enumerate(cols))

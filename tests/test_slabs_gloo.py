@@ -106,3 +106,32 @@ def test_slab_bounds_partition():
             assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 1
     with pytest.raises(ValueError):
         check_slabs(20, 8, 3)
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1804_08968_b200.slabs import broadcast_unique_id
+        uid = broadcast_unique_id(rank)
+        q.put((rank, uid.hex()))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, "ERR " + repr(exc)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_unique_id_broadcast_gloo(world):
+    """The communicator bootstrap of the in-library NCCL transport: rank 0 draws the 128-byte
+    NCCL unique id through the C ABI (dexel_nccl_unique_id; no GPU needed), torch.distributed
+    broadcasts it, and every rank holds the same non-trivial bytes for dexel_nccl_comm_init."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    mp.start_processes(_uid_worker, args=(world, port, q), nprocs=world, join=True, start_method="spawn")
+    res = sorted(q.get() for _ in range(world))
+    ids = {v for _, v in res}
+    assert len(ids) == 1 and not next(iter(ids)).startswith("ERR"), res
+    assert len(bytes.fromhex(next(iter(ids)))) == 128 and int(next(iter(ids)), 16) != 0
