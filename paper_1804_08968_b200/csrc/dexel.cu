@@ -25,6 +25,7 @@
 #include "dexel.h"
 #include "kernels.cuh"
 #include "levels.cuh"
+#include "pass1.cuh"
 #include "pass2.cuh"
 #include "raster.cuh"
 #include "scan.cuh"
@@ -49,7 +50,9 @@ dexel_status fail(dexel_status s, const std::string& msg) {
 #define CK(call)                                                                                  \
   do {                                                                                            \
     cudaError_t e_ = (call);                                                                      \
-    if (e_ != cudaSuccess) return fail(DEXEL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(DEXEL_ECUDA, std::string(#call) + " (dexel.cu:" + std::to_string(__LINE__) + "): " + \
+                                   cudaGetErrorString(e_));                                       \
   } while (0)
 
 struct Buf {
@@ -139,6 +142,7 @@ dexel_status dalloc(dexel_grid g, Buf& b, size_t bytes) {
     cudaError_t e = cudaMallocAsync(&b.p, bytes, g->stream);
     if (e != cudaSuccess) {
       b.p = nullptr;
+      cudaGetLastError();   // (reported here: a caller that recovers must not see it again later)
       return fail(DEXEL_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e) + " (" +
                                     std::to_string(bytes) + " bytes)");
     }
@@ -368,23 +372,56 @@ dexel_status check_radius(float r, double s, int* R) {
 }
 
 // ---------------------------------------------------------------- pass 1
-// one pass-1 launch: main mode over slot rows [jr0, jr0 + nrows_out) of a band whose slot row 0
-// is extended row row0; list mode (nlist >= 0) over the listed tiles
-void launch_p1(int NW, const SrcRows& src, int R, int complement, int row0, int jr0, int nrows_out,
-               const PieceSlots& P, int64_t nlist, const float* prune, cudaStream_t st) {
+// one pass-1 launch of families `fams` (1 = S, 2 = C = U \ S, 3 = both, pass1.cuh): main mode
+// over slot rows [jr0, jr0 + nrows_out) of a band whose slot row 0 is extended row row0; list mode
+// (nlist >= 0, one family) over the listed tiles
+template <int NW, int F, bool TABLE, bool SKIP>
+void launch_p1s_t(unsigned blocks, cudaStream_t st, const SrcRows& src, int R, int row0, int jr0, int nrows_out,
+                  const PieceSlots& PS, const PieceSlots& PC, int64_t nlist, const float* ps, const float* pc) {
+  const size_t smem = p1s_smem();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(p1s_kernel<NW, F, TABLE, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  p1s_kernel<NW, F, TABLE, SKIP><<<blocks, P1_WARPS * 32, smem, st>>>(src, R, row0, jr0, nrows_out, PS, PC, nlist, ps, pc);
+}
+
+template <int F>
+void launch_p1_f(const SrcRows& src, int R, int row0, int jr0, int nrows_out, const PieceSlots& PS,
+                 const PieceSlots& PC, int64_t nlist, const float* ps, const float* pc, cudaStream_t st) {
+  if (R <= P1G_RMAX) {   // gather: a thread per output column (list mode: 32 per listed tile)
+    const int64_t threads = nlist >= 0 ? nlist * 32 : (int64_t)nrows_out * src.nx;
+    const unsigned blocks = (unsigned)((threads + P1G_T - 1) / P1G_T);
+    if (blocks == 0) return;
+#define P1G(RM) p1g_kernel<RM, F><<<blocks, P1G_T, 0, st>>>(src, R, row0, jr0, nrows_out, PS, PC, nlist, ps, pc)
+    if (R <= 1) P1G(1);
+    else if (R == 2) P1G(2);
+    else if (R == 3) P1G(3);
+    else P1G(4);
+#undef P1G
+    return;
+  }
+  // warp sweep: a warp per 32 output columns (list mode: the listed tiles)
   const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
-#define P1(NWV) p1_kernel<NWV, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, jr0, nrows_out, P, nlist, prune)
-  // (skipping sweep steps that change no lane's kappa pays from R = 8; measured)
-  if (NW <= 2 && R < 8)
-    p1_kernel<2, false, false><<<blocks, P1_WARPS * 32, 0, st>>>(src, R, complement, row0, jr0, nrows_out, P, nlist, prune);
-  else if (NW <= 2) P1(2);
-  else if (NW <= 3) P1(3);
-  else if (NW <= 5) P1(5);
-  else if (NW <= 9) P1(9);
-  else P1(17);
-#undef P1
+  const int NW = (32 + 2 * R + 31) / 32;   // window words
+#define P1S(NWV, TB, SK) launch_p1s_t<NWV, F, TB, SK>(blocks, st, src, R, row0, jr0, nrows_out, PS, PC, nlist, ps, pc)
+  if (NW <= 2 && R < 8) P1S(2, true, false);   // (the step-skip vote pays from R = 8, measured)
+  else if (NW <= 2) P1S(2, true, true);
+  else if (NW <= 3) P1S(3, false, true);
+  else if (NW <= 5) P1S(5, false, true);
+  else if (NW <= 9) P1S(9, false, true);
+  else P1S(17, false, true);
+#undef P1S
+}
+
+// single family: complement = 0 -> S into P, 1 -> C into P
+void launch_p1(const SrcRows& src, int R, int complement, int row0, int jr0, int nrows_out, const PieceSlots& P,
+               int64_t nlist, const float* prune, cudaStream_t st) {
+  if (complement) launch_p1_f<2>(src, R, row0, jr0, nrows_out, P, P, nlist, nullptr, prune, st);
+  else launch_p1_f<1>(src, R, row0, jr0, nrows_out, P, P, nlist, prune, nullptr, st);
 }
 
 // Pass-1 launches of band rows [row0, row0 + nrows) (extended numbering), split so that the
@@ -418,7 +455,7 @@ dexel_status p1_setup(dexel_grid g, Temps& T, const SrcRows& src, int nrows, Pie
   *P = PieceSlots{};
   P->nx = src.nx;
   P->nrows = nrows;
-  P->cap = g->p1_cap > 0 ? g->p1_cap : 256;
+  P->cap = (g->p1_cap > 0 ? (g->p1_cap + 3) / 4 * 4 : 256);   // (whole chunks of 4 pieces)
   P->ovf_list_cap = (unsigned)std::max<int64_t>(256, ncol / 64);
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&P->cnt))) return s;
   if ((s = T.get(sizeof(int32_t) * (ncol + 1), (void**)&P->ovf_idx))) return s;
@@ -434,12 +471,12 @@ dexel_status p1_slots(dexel_grid g, Temps& T, const SrcRows& src, int nrows, Pie
   const int64_t ncol = (int64_t)nrows * src.nx;
   const int ntiles = (src.nx + 31) / 32;
   dexel_status s;
-  // the kernels address a column's slots with 32-bit offsets (slot * nx)
-  if ((size_t)(P->cap + 1) * (size_t)src.nx >= ((size_t)1 << 32))
+  // the kernels address a column's chunks with 32-bit offsets (chunk * nx)
+  const size_t nch = (size_t)(P->cap / 4 + 1);   // chunks per column (+ the spill chunk)
+  if (nch * (size_t)src.nx >= ((size_t)1 << 31))
     return fail(DEXEL_EOVERFLOW, "pass-1 slot offsets exceed 32 bits (grid too wide for the piece capacity)");
-  const size_t nslot = (size_t)ncol * (P->cap + 1);
-  if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&P->z))) return s;
-  if ((s = T.get(nslot + 16, (void**)&P->k))) return s;
+  if ((s = T.get(2 * sizeof(float4) * nch * ncol + 32, (void**)&P->z))) return s;
+  if ((s = T.get(sizeof(uint32_t) * nch * ncol + 16, (void**)&P->k))) return s;
   CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
   CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
   CK(cudaMemsetAsync(P->ovf_idx, 0xff, sizeof(int32_t) * (ncol + 1), g->stream));   // -1: slots
@@ -451,7 +488,6 @@ dexel_status p1_slots(dexel_grid g, Temps& T, const SrcRows& src, int nrows, Pie
 dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
                        PieceSlots* P, const unsigned* hf, unsigned long long tot, uint64_t* n_mid,
                        const float* prune, bool* retry) {
-  const int NW = (32 + 2 * R + 31) / 32;
   dexel_status s;
   *retry = false;
   if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
@@ -463,12 +499,12 @@ dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
     return DEXEL_OK;
   }
   if (hf[0] > 0) {
-    P->ovf_cap = (int)hf[1];
-    const size_t na = (size_t)hf[0] * P->ovf_cap;
-    if ((s = T.get(sizeof(float2) * na + 16, (void**)&P->ovf_z))) return s;
-    if ((s = T.get(na + 16, (void**)&P->ovf_k))) return s;
+    P->ovf_cap = (int)((hf[1] + 3) / 4 * 4);   // whole chunks
+    const size_t na = (size_t)hf[0] * (P->ovf_cap / 4);
+    if ((s = T.get(2 * sizeof(float4) * na + 32, (void**)&P->ovf_z))) return s;
+    if ((s = T.get(sizeof(uint32_t) * na + 16, (void**)&P->ovf_k))) return s;
     T.prof.pre(K_P1LIST);
-    launch_p1(NW, src, R, complement, row0, 0, nrows, *P, (int64_t)hf[2], prune, g->stream);
+    launch_p1(src, R, complement, row0, 0, nrows, *P, (int64_t)hf[2], prune, g->stream);
     T.prof.post();
     CK(cudaGetLastError());
     // the list launch adds the arena columns' (filtered) counts to the total
@@ -483,14 +519,13 @@ dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int co
 
 dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
                        PieceSlots* P, uint64_t* n_mid, const float* prune) {
-  const int NW = (32 + 2 * R + 31) / 32;
   dexel_status s;
   if ((s = p1_setup(g, T, src, nrows, P))) return s;
   for (int attempt = 0; attempt < 8; ++attempt) {
     if ((s = p1_slots(g, T, src, nrows, P))) return s;
     CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
       T.prof.pre(K_P1);
-      launch_p1(NW, src, R, complement, row0, jr0, cnt, *P, -1, prune, g->stream);
+      launch_p1(src, R, complement, row0, jr0, cnt, *P, -1, prune, g->stream);
       T.prof.post();
     }));
     unsigned hf[3];
@@ -521,12 +556,8 @@ dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, i
   if ((s = p1_slots(g, T, src, nrows, PA))) return s;
   if ((s = p1_slots(g, T, src, nrows, PB))) return s;
   CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
-    const int64_t warps = (int64_t)cnt * ((src.nx + 31) / 32);
-    const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
-    if (blocks == 0) return;
     T.prof.pre(K_P1);
-    if (R >= 8) p1_dual_kernel<true><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, jr0, cnt, *PA, *PB, prune_a, prune_b);
-    else p1_dual_kernel<false><<<blocks, P1_WARPS * 32, 0, g->stream>>>(src, R, row0, jr0, cnt, *PA, *PB, prune_a, prune_b);
+    launch_p1_f<3>(src, R, row0, jr0, cnt, *PA, *PB, -1, prune_a, prune_b, g->stream);
     T.prof.post();
   }));
   unsigned hf[2][4];
@@ -1022,14 +1053,14 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   const int nx = src->d.nx;
   const int nfam = op == OP_SHELL ? 2 : 1;
   int lcap = src->lev_cap > 0 ? src->lev_cap : 8;
-  // the shell's two pass-1 families in one sweep (p1_dual_kernel) when they share R <= 16 and
-  // both filter (DEXEL_NO_FUSE=1 runs them separately, for testing)
+  // the shell's two pass-1 families in one sweep (pass1.cuh, FAMS = 3) when they share R
+  // (DEXEL_NO_FUSE=1 runs them separately, for testing)
   static const bool no_fuse = [] { const char* e = std::getenv("DEXEL_NO_FUSE"); return e && std::atoi(e); }();
-  const bool fused = op == OP_SHELL && Ra == Rb && Ra <= 16 && prune_a && prune_b && !no_fuse;
+  const bool fused = op == OP_SHELL && Ra == Rb && (prune_a != nullptr) == (prune_b != nullptr) && !no_fuse;
   // bytes per level row of a band: level slots of all families + the piece slots alive at once
   // (one family's, or both when fused)
   const int pcap = src->p1_cap > 0 ? src->p1_cap : 256;
-  size_t row_bytes = (size_t)nx * ((size_t)(pcap + 1) * (sizeof(float2) + 1) + 8) * (fused ? 2 : 1);
+  size_t row_bytes = (size_t)nx * ((size_t)(pcap / 4 + 1) * 36 + 8) * (fused ? 2 : 1);
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
     row_bytes += (size_t)nx * ((Rf + 1) * sizeof(uint16_t) + (Rf + 2) * sizeof(float2) * (size_t)(lcap + 1));
@@ -1191,6 +1222,68 @@ dexel_status run_op(int op, dexel_grid src, float r_a, float r_b, dexel_grid dst
   return s;
 }
 
+// Load every kernel's code now: with CUDA's lazy module loading a kernel is loaded at its first
+// launch, which needs device memory -- and an op's workspace may hold most of it by then (a big
+// op failed its first levels launch with "out of memory").  Once per device, at handle creation.
+template <class K>
+void preload_one(K* fn) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)fn);
+}
+template <int F>
+void preload_p1() {
+  preload_one(p1g_kernel<1, F>);
+  preload_one(p1g_kernel<2, F>);
+  preload_one(p1g_kernel<3, F>);
+  preload_one(p1g_kernel<4, F>);
+  preload_one(p1s_kernel<2, F, true, false>);
+  preload_one(p1s_kernel<2, F, true, true>);
+  preload_one(p1s_kernel<3, F, false, true>);
+  preload_one(p1s_kernel<5, F, false, true>);
+  preload_one(p1s_kernel<9, F, false, true>);
+  preload_one(p1s_kernel<17, F, false, true>);
+}
+template <int OP>
+void preload_p2() {
+  preload_one(pass2s_kernel<OP, 32>);
+  preload_one(pass2s_kernel<OP, 64>);
+  preload_one(pass2s_kernel<OP, 128>);
+}
+void preload_kernels(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  done[device] = true;
+  preload_p1<1>();
+  preload_p1<2>();
+  preload_p1<3>();
+  preload_one(levels_kernel<2>);
+  preload_one(levels_kernel<3>);
+  preload_one(levels_kernel<4>);
+  preload_one(levels_kernel<5>);
+  preload_one(levels_kernel<6>);
+  preload_one(levels_kernel<8>);
+  preload_one(levels_kernel<10>);
+  preload_one(levels_kernel<12>);
+  preload_one(levels_kernel<14>);
+  preload_one(levels_kernel<17>);
+  preload_p2<OP_DILATE>();
+  preload_p2<OP_ERODE>();
+  preload_p2<OP_SHELL>();
+  preload_one(compact_kernel);
+  preload_one(scan_tile_sums);
+  preload_one(scan_sums_exclusive);
+  preload_one(scan_tiles_write);
+  preload_one(validate_kernel);
+  preload_one(rebase_offsets);
+  preload_one(halo_header);
+  preload_one(halo_rebase);
+  preload_one(pieces_to_csr);
+  preload_one(raster_bin_count);
+  preload_one(raster_bin_fill);
+  preload_one(raster_kernel);
+  cudaGetLastError();
+}
+
 }  // namespace
 
 // ================================================================ C ABI
@@ -1217,6 +1310,7 @@ dexel_status dexel_create(const dexel_desc* d, dexel_grid* out) {
   if (d->y0 < 0 || d->y1 > d->ny || d->y0 >= d->y1) return fail(DEXEL_EINVAL, "bad slab rows [y0,y1)");
   if (d->nranks == 1 && (d->y0 != 0 || d->y1 != d->ny)) return fail(DEXEL_EINVAL, "single rank must own all rows");
   CK(cudaSetDevice(d->device));
+  preload_kernels(d->device);
   {
     // keep freed pool memory mapped: ops allocate and free tens of GB per call
     static bool pool_set[64] = {false};

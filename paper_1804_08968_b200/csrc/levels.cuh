@@ -31,6 +31,7 @@
 // active; two half-space sweeps U_f / U_r in separate threads plus a merge ran ~1.5x
 // slower: DESIGN.md "What was tried".)
 //
+// Input: pass-1 piece chunks (kernels.cuh PieceSlots) through a cp.async ring.
 // Layout (HBM): level slots  z[((row*(cap+1) + t)*(R+2) + k)*nx + i]  (float2), t = 1..cap
 // hold L_k ascending (slot 0 is a dummy that absorbs the sweep's first, empty, push), and
 // counts cnt[(row*(R+1) + k)*nx + i] (u16).  For a fixed (row, k, t) the nx columns of a
@@ -99,10 +100,10 @@ struct LvArgs {
 };
 
 constexpr int LV_T = 64;
-constexpr int LV_D = 8;      // pieces per thread in the cp.async ring
+constexpr int LV_DC = 3;     // piece chunks (4 pieces each) per thread in the cp.async ring
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
 }
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
@@ -131,7 +132,7 @@ struct LvTab {
 };
 
 template <int LMAX>
-__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs A) {
+__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 6 : 8) levels_kernel(LvArgs A) {
   constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
   __shared__ __align__(16) float Hs[257 * HS];   // h(kappa, k0 + k), NaN beyond R or out of reach;
                                                   // row R+1: all NaN (the "null piece")
@@ -142,13 +143,16 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     const float h = (kap <= R && kk < LMAX && k <= R) ? A.h[kap * L1 + k] : -1.0f;
     Hs[t] = h >= 0.f ? h : __int_as_float(0x7fc00000);   // quiet NaN
   }
-  __shared__ float2 ringz[LV_D][LV_T];
-  __shared__ uint32_t ringk[LV_D][LV_T];
+  // pieces stream through a per-thread ring of LV_DC chunks (4 pieces = 32 bytes of z pairs as two
+  // float4 halves + the 32-bit word of their kappa bytes) filled by cp.async: LV_DC - 1 chunks in
+  // flight per thread, no registers held
+  __shared__ float4 ringz[LV_DC][2][LV_T];
+  __shared__ uint32_t ringk[LV_DC][LV_T];
   __syncthreads();
   uint32_t tot = 0, mx = 0;
   const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
   const bool live = g < (A.list ? A.nlist : A.ncol);
-  // every lane of the warp walks the same piece index t = 0..mmax-1: the slot reads stay
+  // every lane of the warp walks the same piece index t = 0..mmax-1: the chunk reads stay
   // coalesced and the loop never diverges; a lane past its own count processes the "null
   // piece" (kappa row R+1, all NaN), which leaves the sweep unchanged
   const int m = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
@@ -160,19 +164,20 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   const int64_t c = live ? (A.list ? (int64_t)A.list[g] : g) : 0;
   const int q = A.list ? (int)g : -1;
   const int row = (int)(c / A.L.nx), i = (int)(c % A.L.nx);
-  // this column's pieces: slots (stride nx, coalesced across the warp) or the overflow arena
-  const float2* zc;
-  const uint8_t* kc;
-  int64_t ps;
+  // this column's piece chunks: slots (chunk stride nx, coalesced across the warp) or the
+  // pass-1 overflow arena (stride 1)
+  const float4* zc;
+  const uint32_t* kc;
+  int64_t cstr;
   if (m <= A.P.cap) {   // (a column's pieces live in the arena exactly when it has more than cap)
-    zc = A.P.z + piece_index(A.P, row, 0, i);
-    kc = A.P.k + piece_index(A.P, row, 0, i);
-    ps = A.P.nx;
+    zc = A.P.z + 2 * chunk_index(A.P, row, 0, i);
+    kc = A.P.k + chunk_index(A.P, row, 0, i);
+    cstr = A.P.nx;
   } else {
-    const size_t qo = (size_t)A.P.ovf_idx[c] * A.P.ovf_cap;
-    zc = A.P.ovf_z + qo;
+    const size_t qo = (size_t)A.P.ovf_idx[c] * (A.P.ovf_cap / 4);
+    zc = A.P.ovf_z + 2 * qo;
     kc = A.P.ovf_k + qo;
-    ps = 1;
+    cstr = 1;
   }
   // main pass: slots of (row, level k0); overflow pass: the arena lists of slot q.
   // o[k] = offset (float2) of the next free slot of level k0+k from Zd; slot 0 is the dummy.
@@ -193,30 +198,33 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     pce[k] = -INFINITY;   // no previous component
     o[k] = (uint32_t)k * olev;
   }
-  // pieces stream through a per-thread ring of LV_D shared-memory slots filled by cp.async
-  // (LV_D - 1 pieces in flight per thread, no registers held): z as 8 bytes, kappa as the
-  // aligned 4-byte word that holds it
-  auto issue = [&](int t) {
-    if (t < m) {
-      const int u = t % LV_D;
-      const uint8_t* kp = kc + (int64_t)t * ps;
-      cp_async8(&ringz[u][threadIdx.x], zc + (int64_t)t * ps);
-      cp_async4(&ringk[u][threadIdx.x], reinterpret_cast<const uint32_t*>((uintptr_t)kp & ~(uintptr_t)3));
+  const int nchunk = (m + 3) >> 2;
+  auto issue = [&](int cq) {
+    if (cq < nchunk) {
+      const int u = cq % LV_DC;
+      const float4* src = zc + 2 * (int64_t)cq * cstr;
+      cp_async16(&ringz[u][0][threadIdx.x], src);
+      cp_async16(&ringz[u][1][threadIdx.x], src + 1);
+      cp_async4(&ringk[u][threadIdx.x], kc + (int64_t)cq * cstr);
     }
     cp_async_commit();   // (empty groups too: the wait count stays uniform)
   };
 #pragma unroll
-  for (int t = 0; t < LV_D - 1; ++t) issue(t);
+  for (int t = 0; t < LV_DC - 1; ++t) issue(t);
+  uint32_t kw = 0;
   for (int t = 0; t < mmax; ++t) {
-    issue(t + LV_D - 1);
-    cp_async_wait<LV_D - 1>();        // piece t has landed (this thread's own copies)
+    const int u = (t >> 2) % LV_DC;
+    if ((t & 3) == 0) {
+      issue((t >> 2) + LV_DC - 1);
+      cp_async_wait<LV_DC - 1>();     // chunk t/4 has landed (this thread's own copies)
+      kw = ringk[u][threadIdx.x];
+    }
     float2 p = make_float2(0.f, 0.f);
     int nk = L1;                      // past the column's pieces: the null piece
     if (t < m) {
-      const int u = t % LV_D;
-      p = ringz[u][threadIdx.x];
-      const uintptr_t ka = (uintptr_t)(kc + (int64_t)t * ps);
-      nk = (int)((ringk[u][threadIdx.x] >> (8u * (uint32_t)(ka & 3))) & 0xffu);
+      const float2* half = reinterpret_cast<const float2*>(&ringz[u][(t >> 1) & 1][threadIdx.x]);
+      p = half[t & 1];
+      nk = (int)((kw >> (8u * (uint32_t)(t & 3))) & 0xffu);
     }
     const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
     float hv[4 * NV];
