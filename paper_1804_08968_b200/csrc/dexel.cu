@@ -93,6 +93,15 @@ struct dexel_grid_s {
   bool halo_pending = false;
   std::vector<int32_t> part;   // NCCL: every rank's slab rows (y0, y1), gathered on first use
   Buf hdr;                     // NCCL: interval counts sent [0..1] / received [2..3]
+  // device h(kappa, k) tables of the last radii used (make_htab), with the host copies their
+  // asynchronous uploads read from: a repeated op uploads nothing and waits for nothing
+  struct HTab {
+    float r = -1.f;
+    double s = 0.0;
+    Buf dev;
+    std::vector<float> host;
+  } htab[2];
+  int htab_next = 0;
 };
 
 namespace {
@@ -357,6 +366,24 @@ dexel_status scan_counts(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n
   return DEXEL_OK;
 }
 
+// exclusive scan of cnt[0..n) into off[0..n], the total at off[n] (stays on the device)
+dexel_status scan_counts_dev(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n, uint64_t* off) {
+  const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (n == 0) {
+    CK(cudaMemsetAsync(off, 0, sizeof(uint64_t), g->stream));
+    return DEXEL_OK;
+  }
+  uint64_t* sums = nullptr;
+  dexel_status s = T.get(sizeof(uint64_t) * (ntiles + 2), (void**)&sums);
+  if (s) return s;
+  LAUNCH(T, K_SCAN, scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums));
+  LAUNCH(T, K_SCAN, scan_sums_exclusive<<<1, SCAN_THREADS, 0, g->stream>>>(sums, ntiles));
+  LAUNCH(T, K_SCAN, scan_tiles_write<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums, off));
+  CK(cudaGetLastError());
+  T.release(sums);
+  return DEXEL_OK;
+}
+
 int radius_levels(double r, double s) {
   int R = (int)std::floor(r / s);
   while ((double)(R + 1) * s <= r) ++R;
@@ -389,9 +416,12 @@ void launch_p1s_t(unsigned blocks, cudaStream_t st, const SrcRows& src, int R, i
 
 template <int F>
 void launch_p1_f(const SrcRows& src, int R, int row0, int jr0, int nrows_out, const PieceSlots& PS,
-                 const PieceSlots& PC, int64_t nlist, const float* ps, const float* pc, cudaStream_t st) {
+                 const PieceSlots& PC, int64_t nlist, const float* ps, const float* pc, cudaStream_t st,
+                 int64_t list_warps = 0) {
+  // (list mode, nlist >= 0: nlist is the tile list's capacity, the kernels read the live count;
+  // list_warps warps walk it grid-stride)
   if (R <= P1G_RMAX) {   // gather: a thread per output column (list mode: 32 per listed tile)
-    const int64_t threads = nlist >= 0 ? nlist * 32 : (int64_t)nrows_out * src.nx;
+    const int64_t threads = nlist >= 0 ? list_warps * 32 : (int64_t)nrows_out * src.nx;
     const unsigned blocks = (unsigned)((threads + P1G_T - 1) / P1G_T);
     if (blocks == 0) return;
 #define P1G(RM) p1g_kernel<RM, F><<<blocks, P1G_T, 0, st>>>(src, R, row0, jr0, nrows_out, PS, PC, nlist, ps, pc)
@@ -403,7 +433,7 @@ void launch_p1_f(const SrcRows& src, int R, int row0, int jr0, int nrows_out, co
     return;
   }
   // warp sweep: a warp per 32 output columns (list mode: the listed tiles)
-  const int64_t warps = nlist >= 0 ? nlist : (int64_t)nrows_out * ((src.nx + 31) / 32);
+  const int64_t warps = nlist >= 0 ? list_warps : (int64_t)nrows_out * ((src.nx + 31) / 32);
   const unsigned blocks = (unsigned)((warps + P1_WARPS - 1) / P1_WARPS);
   if (blocks == 0) return;
   const int NW = (32 + 2 * R + 31) / 32;   // window words
@@ -419,9 +449,9 @@ void launch_p1_f(const SrcRows& src, int R, int row0, int jr0, int nrows_out, co
 
 // single family: complement = 0 -> S into P, 1 -> C into P
 void launch_p1(const SrcRows& src, int R, int complement, int row0, int jr0, int nrows_out, const PieceSlots& P,
-               int64_t nlist, const float* prune, cudaStream_t st) {
-  if (complement) launch_p1_f<2>(src, R, row0, jr0, nrows_out, P, P, nlist, nullptr, prune, st);
-  else launch_p1_f<1>(src, R, row0, jr0, nrows_out, P, P, nlist, prune, nullptr, st);
+               int64_t nlist, const float* prune, cudaStream_t st, int64_t list_warps = 0) {
+  if (complement) launch_p1_f<2>(src, R, row0, jr0, nrows_out, P, P, nlist, nullptr, prune, st, list_warps);
+  else launch_p1_f<1>(src, R, row0, jr0, nrows_out, P, P, nlist, prune, nullptr, st, list_warps);
 }
 
 // Pass-1 launches of band rows [row0, row0 + nrows) (extended numbering), split so that the
@@ -444,11 +474,12 @@ cudaError_t launch_rows_split(dexel_grid g, const SrcRows& src, int row0, int nr
   return cudaGetLastError();
 }
 
-// Pass 1 over rows [row0, row0+nrows) of src: pieces into per-column slots (one launch);
-// columns with more than cap pieces are recomputed into an arena sized from the longest
-// column (a second, tile-list launch); too many of them doubles cap and reruns.
-// p1_setup: the fixed per-band buffers; p1_slots: the slot arrays of one attempt (+ flag reset)
-dexel_status p1_setup(dexel_grid g, Temps& T, const SrcRows& src, int nrows, PieceSlots* P) {
+// Pass 1 over band rows [row0, row0+nrows) of src: pieces into per-column slots (one launch, split
+// around the halo rows), then the list launch that recomputes the columns that outgrew their slots
+// into the arena -- launched unconditionally: it reads the listed-tile count on the device, so the
+// host never waits here.  A column that fits neither (too many listed, or longer than the arena
+// lists) raises OPF_P1_RERUN; the op's one readback reruns it with larger slots (run_op_impl).
+dexel_status p1_alloc(dexel_grid g, Temps& T, const SrcRows& src, int nrows, unsigned* opf, PieceSlots* P) {
   const int64_t ncol = (int64_t)nrows * src.nx;
   const int ntiles = (src.nx + 31) / 32;
   dexel_status s;
@@ -456,133 +487,74 @@ dexel_status p1_setup(dexel_grid g, Temps& T, const SrcRows& src, int nrows, Pie
   P->nx = src.nx;
   P->nrows = nrows;
   P->cap = (g->p1_cap > 0 ? (g->p1_cap + 3) / 4 * 4 : 256);   // (whole chunks of 4 pieces)
+  // the arena: up to 1/64 of the columns, 4x the slot capacity each (beyond: the op reruns with
+  // larger slots -- a memory trade: larger slots for every column cost more bands)
   P->ovf_list_cap = (unsigned)std::max<int64_t>(256, ncol / 64);
+  P->ovf_cap = 4 * P->cap;                                    // arena pieces per listed column
+  P->opf = opf;
+  P->total = reinterpret_cast<unsigned long long*>(opf + 8);   // n_mid
+  // the kernels address a column's chunks with 32-bit offsets (chunk * nx)
+  const size_t nch = (size_t)(P->cap / 4 + 1);   // chunks per column (+ the spill chunk)
+  if (nch * 4 * (size_t)src.nx >= ((size_t)1 << 31))
+    return fail(DEXEL_EOVERFLOW, "pass-1 slot offsets exceed 32 bits (grid too wide for the piece capacity)");
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&P->cnt))) return s;
   if ((s = T.get(sizeof(int32_t) * (ncol + 1), (void**)&P->ovf_idx))) return s;
   if ((s = T.get(64, (void**)&P->flags))) return s;
-  P->total = (unsigned long long*)(P->flags + 8);
   if ((s = T.get(sizeof(uint32_t) * P->ovf_list_cap * 2, (void**)&P->ovf_list))) return s;
   P->tile_list = P->ovf_list + P->ovf_list_cap;
   if ((s = T.get(sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), (void**)&P->tile_flag))) return s;
-  return DEXEL_OK;
-}
-
-dexel_status p1_slots(dexel_grid g, Temps& T, const SrcRows& src, int nrows, PieceSlots* P) {
-  const int64_t ncol = (int64_t)nrows * src.nx;
-  const int ntiles = (src.nx + 31) / 32;
-  dexel_status s;
-  // the kernels address a column's chunks with 32-bit offsets (chunk * nx)
-  const size_t nch = (size_t)(P->cap / 4 + 1);   // chunks per column (+ the spill chunk)
-  if (nch * (size_t)src.nx >= ((size_t)1 << 31))
-    return fail(DEXEL_EOVERFLOW, "pass-1 slot offsets exceed 32 bits (grid too wide for the piece capacity)");
   if ((s = T.get(2 * sizeof(float4) * nch * ncol + 32, (void**)&P->z))) return s;
   if ((s = T.get(sizeof(uint32_t) * nch * ncol + 16, (void**)&P->k))) return s;
+  const size_t na = (size_t)P->ovf_list_cap * (P->ovf_cap / 4);
+  if ((s = T.get(2 * sizeof(float4) * na + 32, (void**)&P->ovf_z))) return s;
+  if ((s = T.get(sizeof(uint32_t) * na + 16, (void**)&P->ovf_k))) return s;
   CK(cudaMemsetAsync(P->flags, 0, 64, g->stream));
   CK(cudaMemsetAsync(P->tile_flag, 0, sizeof(uint32_t) * ((size_t)nrows * ntiles + 1), g->stream));
   CK(cudaMemsetAsync(P->ovf_idx, 0xff, sizeof(int32_t) * (ncol + 1), g->stream));   // -1: slots
   return DEXEL_OK;
 }
 
-// after a main launch: hf = flags[0..2], tot = total.  Returns DEXEL_OK with *retry set when
-// too many columns overflowed (the caller doubles cap and reruns), else runs the list launch.
-dexel_status p1_finish(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
-                       PieceSlots* P, const unsigned* hf, unsigned long long tot, uint64_t* n_mid,
-                       const float* prune, bool* retry) {
-  dexel_status s;
-  *retry = false;
-  if (hf[0] > P->ovf_list_cap) {   // many long columns: larger slots pay
-    T.release(P->z);
-    T.release(P->k);
-    P->cap *= 2;
-    g->p1_cap = P->cap;
-    *retry = true;
-    return DEXEL_OK;
-  }
-  if (hf[0] > 0) {
-    P->ovf_cap = (int)((hf[1] + 3) / 4 * 4);   // whole chunks
-    const size_t na = (size_t)hf[0] * (P->ovf_cap / 4);
-    if ((s = T.get(2 * sizeof(float4) * na + 32, (void**)&P->ovf_z))) return s;
-    if ((s = T.get(sizeof(uint32_t) * na + 16, (void**)&P->ovf_k))) return s;
-    T.prof.pre(K_P1LIST);
-    launch_p1(src, R, complement, row0, 0, nrows, *P, (int64_t)hf[2], prune, g->stream);
-    T.prof.post();
-    CK(cudaGetLastError());
-    // the list launch adds the arena columns' (filtered) counts to the total
-    Readback rb{g};
-    rb.add(0, P->total, sizeof(tot));
-    CK(rb.wait());
-    rb.get(0, &tot, sizeof(tot));
-  }
-  *n_mid += tot;
-  return DEXEL_OK;
+// the list launch: a fixed grid walks the listed tiles (count read on the device)
+void p1_list_launch(Temps& T, const SrcRows& src, int R, int fams, int row0, const PieceSlots& PS,
+                    const PieceSlots& PC, const float* ps, const float* pc, cudaStream_t st) {
+  const unsigned nl = (fams == 2 ? PC : PS).ovf_list_cap;   // the tile list's capacity
+  const int64_t cap_warps = std::min<int64_t>(nl, 148 * 16);
+  T.prof.pre(K_P1LIST);
+  if (fams == 1) launch_p1_f<1>(src, R, row0, 0, 0, PS, PC, (int64_t)nl, ps, pc, st, cap_warps);
+  else launch_p1_f<2>(src, R, row0, 0, 0, PS, PC, (int64_t)nl, ps, pc, st, cap_warps);
+  T.prof.post();
 }
 
 dexel_status run_pass1(dexel_grid g, Temps& T, const SrcRows& src, int R, int complement, int row0, int nrows,
-                       PieceSlots* P, uint64_t* n_mid, const float* prune) {
+                       unsigned* opf, PieceSlots* P, const float* prune) {
   dexel_status s;
-  if ((s = p1_setup(g, T, src, nrows, P))) return s;
-  for (int attempt = 0; attempt < 8; ++attempt) {
-    if ((s = p1_slots(g, T, src, nrows, P))) return s;
-    CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
-      T.prof.pre(K_P1);
-      launch_p1(src, R, complement, row0, jr0, cnt, *P, -1, prune, g->stream);
-      T.prof.post();
-    }));
-    unsigned hf[3];
-    unsigned long long tot = 0;
-    {
-      Readback rb{g};
-      rb.add(0, P->flags, sizeof(hf));
-      rb.add(16, P->total, sizeof(tot));
-      CK(rb.wait());
-      rb.get(0, hf, sizeof(hf));
-      rb.get(16, &tot, sizeof(tot));
-    }
-    bool retry = false;
-    if ((s = p1_finish(g, T, src, R, complement, row0, nrows, P, hf, tot, n_mid, prune, &retry))) return s;
-    if (!retry) return DEXEL_OK;
-  }
-  return fail(DEXEL_ECUDA, "pass-1 slot sizing did not converge");
+  if ((s = p1_alloc(g, T, src, nrows, opf, P))) return s;
+  CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
+    T.prof.pre(K_P1);
+    launch_p1(src, R, complement, row0, jr0, cnt, *P, -1, prune, g->stream);
+    T.prof.post();
+  }));
+  p1_list_launch(T, src, R, complement ? 2 : 1, row0, *P, *P, complement ? nullptr : prune, complement ? prune : nullptr,
+                 g->stream);
+  CK(cudaGetLastError());
+  return DEXEL_OK;
 }
 
-// both shell families (S at r_a, C = U \ S at r_b, the same R <= 16) in one sweep
-// (p1_dual_kernel); a family whose slots overflow too often is redone alone by run_pass1
-dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, int row0, int nrows,
-                            PieceSlots* PA, PieceSlots* PB, uint64_t* n_mid, const float* prune_a,
-                            const float* prune_b) {
+// both shell families (S at r_a, C = U \ S at r_b, the same R) in one sweep (FAMS = 3); the
+// overflow columns are redone per family in list mode
+dexel_status run_pass1_dual(dexel_grid g, Temps& T, const SrcRows& src, int R, int row0, int nrows, unsigned* opf,
+                            PieceSlots* PA, PieceSlots* PB, const float* prune_a, const float* prune_b) {
   dexel_status s;
-  if ((s = p1_setup(g, T, src, nrows, PA))) return s;
-  if ((s = p1_setup(g, T, src, nrows, PB))) return s;
-  if ((s = p1_slots(g, T, src, nrows, PA))) return s;
-  if ((s = p1_slots(g, T, src, nrows, PB))) return s;
+  if ((s = p1_alloc(g, T, src, nrows, opf, PA))) return s;
+  if ((s = p1_alloc(g, T, src, nrows, opf, PB))) return s;
   CK(launch_rows_split(g, src, row0, nrows, [&](int jr0, int cnt) {
     T.prof.pre(K_P1);
     launch_p1_f<3>(src, R, row0, jr0, cnt, *PA, *PB, -1, prune_a, prune_b, g->stream);
     T.prof.post();
   }));
-  unsigned hf[2][4];
-  unsigned long long tot[2] = {0, 0};
-  {
-    Readback rb{g};
-    rb.add(0, PA->flags, 3 * sizeof(unsigned));
-    rb.add(16, PA->total, sizeof(tot[0]));
-    rb.add(32, PB->flags, 3 * sizeof(unsigned));
-    rb.add(48, PB->total, sizeof(tot[1]));
-    CK(rb.wait());
-    rb.get(0, hf[0], 3 * sizeof(unsigned));
-    rb.get(16, &tot[0], sizeof(tot[0]));
-    rb.get(32, hf[1], 3 * sizeof(unsigned));
-    rb.get(48, &tot[1], sizeof(tot[1]));
-  }
-  for (int f = 0; f < 2; ++f) {
-    PieceSlots* P = f ? PB : PA;
-    const float* prune = f ? prune_b : prune_a;
-    bool retry = false;
-    if ((s = p1_finish(g, T, src, R, f, row0, nrows, P, hf[f], tot[f], n_mid, prune, &retry))) return s;
-    if (retry) {   // rare: this family alone, with grown slots
-      if ((s = run_pass1(g, T, src, R, f, row0, nrows, P, n_mid, prune))) return s;
-    }
-  }
+  p1_list_launch(T, src, R, 1, row0, *PA, *PA, prune_a, nullptr, g->stream);
+  p1_list_launch(T, src, R, 2, row0, *PB, *PB, nullptr, prune_b, g->stream);
+  CK(cudaGetLastError());
   return DEXEL_OK;
 }
 
@@ -596,9 +568,21 @@ void release_pieces(Temps& T, PieceSlots& P) {
 // to fp32 (readings R10, R20), -1 where kappa^2 + k^2 > (r/s)^2: the device never
 // evaluates a square root of a weight, and which (kappa, k) contribute is decided exactly.
 dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, float** prune) {
+  (void)T;
   const double s = g->d.spacing;
   const int n1 = R + 1;
-  std::vector<float> h((size_t)n1 * n1);
+  const char* e = std::getenv("DEXEL_NO_PRUNE");
+  const bool no_prune = e && std::atoi(e);
+  const size_t nh = (size_t)n1 * n1;
+  for (auto& H : g->htab)   // the same radius as a recent op: nothing to build, upload or wait for
+    if (H.dev.p && H.r == r && H.s == s) {
+      *out = (float*)H.dev.p;
+      *prune = no_prune ? nullptr : *out + nh;
+      return DEXEL_OK;
+    }
+  dexel_grid_s::HTab& H = g->htab[g->htab_next];
+  g->htab_next ^= 1;
+  std::vector<float> h(nh + n1 + 1);
   const double rr = (double)r * (double)r;
   for (int a = 0; a < n1; ++a)
     for (int k = 0; k < n1; ++k) {
@@ -607,50 +591,64 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
     }
   // capsule-domination table for the pass-1 filter: h(kappa, 0), rounded once to fp32
   // (DEXEL_NO_PRUNE=1 disables the filter)
-  // (+ one entry: the absolute part of the domination margin, 16 r 2^-24 >= 4 ulp(r), kernels.cuh)
-  std::vector<float> h0(n1 + 1);
-  for (int a = 0; a < n1; ++a) h0[a] = (float)std::sqrt(std::max(0.0, rr - (double)a * a * s * s));
-  h0[n1] = (float)(16.0 * (double)r * std::ldexp(1.0, -24));
+  // (+ one entry: the absolute part of the domination margin, 16 r 2^-24 >= 8 ulp(r), kernels.cuh)
+  for (int a = 0; a < n1; ++a) h[nh + a] = (float)std::sqrt(std::max(0.0, rr - (double)a * a * s * s));
+  h[nh + n1] = (float)(16.0 * (double)r * std::ldexp(1.0, -24));
   dexel_status st;
-  if ((st = T.get(sizeof(float) * (h.size() + n1 + 1) + 16, (void**)out))) return st;
-  float* d0 = *out + h.size();
-  CK(cudaMemcpyAsync(*out, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, g->stream));
-  CK(cudaMemcpyAsync(d0, h0.data(), sizeof(float) * (n1 + 1), cudaMemcpyHostToDevice, g->stream));
-  CK(timed_sync(g->stream));  // the host vectors go out of scope
-  const char* e = std::getenv("DEXEL_NO_PRUNE");
-  *prune = (e && std::atoi(e)) ? nullptr : d0;
+  dfree(g, H.dev);   // (stream-ordered after the ops that used it)
+  H.r = -1.f;
+  if ((st = dalloc(g, H.dev, sizeof(float) * h.size() + 16))) return st;
+  H.host.swap(h);
+  // the host copy stays alive with the cache entry; the upload is stream-ordered, no wait
+  CK(cudaMemcpyAsync(H.dev.p, H.host.data(), sizeof(float) * H.host.size(), cudaMemcpyHostToDevice, g->stream));
+  H.r = r;
+  H.s = s;
+  *out = (float*)H.dev.p;
+  *prune = no_prune ? nullptr : *out + nh;
   return DEXEL_OK;
 }
 
 // level slots of one family for level rows [lr0, lr0 + lrn) (extended-row numbering):
-// pass 1 on those rows, then the level-set kernel; the pieces are freed on return.
-// A level list longer than the slot capacity reruns the level kernel with a larger cap.
-// (pre != nullptr: the family's pieces were computed already, by run_pass1_dual)
+// pass 1 on those rows, then the level-set kernel and its overflow pass (launched unconditionally:
+// it reads the listed-column count on the device); the pieces are freed on return.  A list that
+// fits neither its slots nor the arena raises OPF_LV_RERUN (the op's readback reruns it with a
+// larger level capacity).  (pre != nullptr: the family's pieces were computed already, by
+// run_pass1_dual)
 dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, const float* prune,
-                        int complement, int lr0, int lrn, LevelSlots* L, uint64_t* n_mid, uint64_t* n_lev,
+                        int complement, int lr0, int lrn, unsigned* opf, LevelSlots* L,
                         const PieceSlots* pre = nullptr, bool slices = false) {
   // slices: only L_0 is needed (pass 2 reads dy = 0), so only the first chunk of levels runs
   const int nlev_compute = slices ? 1 : R + 1;
   dexel_status s;
   PieceSlots P;
   if (pre) P = *pre;
-  else if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, &P, n_mid, prune))) return s;
+  else if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, opf, &P, prune))) return s;
   const int64_t ncol = (int64_t)lrn * src.nx;
   unsigned* flags = nullptr;
   if ((s = T.get(64, (void**)&flags))) return s;
-  unsigned long long* nlev = (unsigned long long*)(flags + 8);
+  unsigned long long* nlev = reinterpret_cast<unsigned long long*>(opf + 10);
   L->R = R;
   L->ry = slices ? 0 : R;
   L->nx = src.nx;
   L->nrows = lrn;
   L->row0 = lr0;
   L->cap = g->lev_cap > 0 ? g->lev_cap : 8;
+  // arena lists: 4x the slot capacity (at least 32); longer lists rerun the op with larger slots
+  L->ovf_cap = std::min(LV_CNT_MAX, std::max(32, 4 * L->cap));
   const size_t nlist = (size_t)ncol * (R + 1);
   if ((s = T.get(sizeof(uint16_t) * nlist + 16, (void**)&L->cnt))) return s;
   if ((s = T.get(sizeof(int32_t) * ncol + 16, (void**)&L->ovf_idx))) return s;
-  const unsigned ovf_cap = (unsigned)std::max<int64_t>(256, ncol / 256);
+  const unsigned ovf_list_cap = (unsigned)std::max<int64_t>(256, ncol / 256);
   uint32_t* ovf_list = nullptr;
-  if ((s = T.get(sizeof(uint32_t) * ovf_cap, (void**)&ovf_list))) return s;
+  if ((s = T.get(sizeof(uint32_t) * ovf_list_cap, (void**)&ovf_list))) return s;
+  const size_t nslot = (size_t)ncol * (R + 2) * (L->cap + 1);   // + the dummy slot, the spill level
+  if ((size_t)(R + 2) * (L->cap + 1) * src.nx >= (1ull << 32))
+    return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
+  if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
+  if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * (R + 1) * (L->ovf_cap + 1) + 16, (void**)&L->ovf_z)))
+    return s;
+  CK(cudaMemsetAsync(flags, 0, 64, g->stream));
+  CK(cudaMemsetAsync(L->ovf_idx, 0xff, sizeof(int32_t) * ncol, g->stream));   // -1: no arena slot
   // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of
   // <= max_chunk (larger chunks cost more in registers/occupancy than they save)
   static const int kChunk[] = {2, 3, 4, 5, 6, 8, 10, 12, 14, 17};
@@ -672,60 +670,21 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
     }
     T.prof.post();
   };
-  for (int attempt = 0; attempt < 6; ++attempt) {
-    const size_t nslot = (size_t)ncol * (R + 2) * (L->cap + 1);   // + the dummy slot, the spill level
-    if ((size_t)(R + 2) * (L->cap + 1) * src.nx >= (1ull << 32))
-      return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
-    if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
-    CK(cudaMemsetAsync(flags, 0, 64, g->stream));
-    CK(cudaMemsetAsync(L->ovf_idx, 0xff, sizeof(int32_t) * ncol, g->stream));   // -1: no arena slot
-    static const bool dbg_on = std::getenv("DEXEL_DEBUG") != nullptr;
-    unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
-    LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_cap, nullptr, 0};
-    launch(A, ncol);
-    CK(cudaGetLastError());
-    unsigned hf[3];
-    unsigned long long hn = 0;
-    {
-      Readback rb{g};
-      rb.add(0, flags, sizeof(hf));
-      rb.add(16, nlev, sizeof(hn));
-      CK(rb.wait());
-      rb.get(0, hf, sizeof(hf));
-      rb.get(16, &hn, sizeof(hn));
-    }
-    if (dbg) {
-      unsigned long long hd[2];
-      CK(cudaMemcpy(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost));
-      unsigned long long tm = 0;
-      CK(cudaMemcpy(&tm, P.total, sizeof(tm), cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "[dexel] levels rows %d..%d: %llu pieces, %lld columns (mean %.1f), warps %llu, mean warp max %.1f\n",
-                   lr0, lr0 + lrn, tm, (long long)ncol, (double)tm / ncol, hd[1], (double)hd[0] / std::max(1ull, hd[1]));
-    }
-    if (hf[1] <= ovf_cap) {
-      if (hf[1] > 0) {   // overflow pass: the listed columns' lists, all of them, into the arena
-        // arena lists of the most pieces any listed column has (a list never holds more)
-        L->ovf_cap = (int)std::max(hf[2], 1u);
-        if (L->ovf_cap > LV_CNT_MAX)
-          return fail(DEXEL_EOVERFLOW, "a column has more than " + std::to_string(LV_CNT_MAX) +
-                                           " pass-1 pieces (level lists are counted in 15 bits)");
-        if ((s = T.get(sizeof(float2) * (size_t)hf[1] * (R + 1) * (L->ovf_cap + 1) + 16, (void**)&L->ovf_z)))
-          return s;
-        LvArgs B = A;
-        B.L = *L;
-        B.list = ovf_list;
-        B.nlist = hf[1];
-        launch(B, hf[1]);
-        CK(cudaGetLastError());
-      }
-      *n_lev += hn;   // (the overflow pass adds nothing to the count)
-      break;
-    }
-    // too many long lists: a larger slot capacity pays
-    T.release(L->z);
-    L->cap = std::min(LV_SLOT_MAX, 2 * L->cap);
-    g->lev_cap = L->cap;
-    if (attempt == 5) return fail(DEXEL_ECUDA, "level capacity sizing did not converge");
+  static const bool dbg_on = std::getenv("DEXEL_DEBUG") != nullptr;
+  unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
+  LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_list_cap, nullptr, opf};
+  launch(A, ncol);
+  // the overflow pass: every listed column's lists into the arena (a fixed grid, grid-stride over
+  // the count the main pass left on the device)
+  LvArgs B = A;
+  B.list = ovf_list;
+  launch(B, std::min<int64_t>(ovf_list_cap, 148 * 8 * LV_T));
+  CK(cudaGetLastError());
+  if (dbg) {   // (diagnostics only: waits)
+    unsigned long long hd[2];
+    CK(cudaMemcpy(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[dexel] levels rows %d..%d: %lld columns, warps %llu, mean warp max %.1f pieces\n",
+                 lr0, lr0 + lrn, (long long)ncol, hd[1], (double)hd[0] / std::max(1ull, hd[1]));
   }
   release_pieces(T, P);
   T.release(ovf_list);
@@ -1099,44 +1058,40 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
     const int nb = (src->nrows + band - 1) / band;
     band = (src->nrows + nb - 1) / nb;
   }
-  stats.lev_cap = 0;
   uint32_t* ocnt = nullptr;
-  unsigned* flags = nullptr;
+  unsigned* opf = nullptr;   // the op's flag words and statistics (kernels.cuh OpFlag)
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
-  if ((s = T.get(64, (void**)&flags))) return s;
+  if ((s = T.get(sizeof(unsigned) * OPF_WORDS, (void**)&opf))) return s;
   int acc = src->p2_acc > 0 ? src->p2_acc : 32;
   float2* stage = nullptr;
+  // Every capacity of the op (piece slots and arena, level slots and arena, the pass-2
+  // accumulator, dst's buffer) is checked ONCE, at the end: kernels raise flags instead of the
+  // host reading sizes back after every launch.  The one readback (flags + statistics + the
+  // output size) then either confirms the op or grows what overflowed and reruns it.
   for (int attempt = 0;; ++attempt) {
+    const int nb = (src->nrows + band - 1) / band;
     if ((s = T.get(sizeof(float2) * (size_t)pass2_stage_cap(op, acc) * ncol + 16, (void**)&stage))) return s;
-    CK(cudaMemsetAsync(flags, 0, 64, st));
-    stats.n_mid = 0;
-    stats.n_lev = 0;
+    CK(cudaMemsetAsync(opf, 0, sizeof(unsigned) * OPF_WORDS, st));
+    uint32_t lev_cap_used = 0;
     for (int b0 = 0; b0 < src->nrows; b0 += band) {
       const int b1 = std::min(src->nrows, b0 + band);
       const int lr0 = std::max(0, hlo + b0 - Rmax), lr1 = std::min(nrows_ext, hlo + b1 + Rmax);
       LevelSlots LA{}, LB{};
       PieceSlots PA{}, PB{};
-      if (fused && (s = run_pass1_dual(src, T, rows, Ra, lr0, lr1 - lr0, &PA, &PB, &stats.n_mid, prune_a, prune_b))) {
-        set_empty(dst);
-        return s;
-      }
+      if (fused && (s = run_pass1_dual(src, T, rows, Ra, lr0, lr1 - lr0, opf, &PA, &PB, prune_a, prune_b))) return s;
       // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
-      if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, &LA, &stats.n_mid,
-                          &stats.n_lev, fused ? &PA : nullptr, slices))) {
-        set_empty(dst);
+      if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, opf, &LA,
+                          fused ? &PA : nullptr, slices)))
         return s;
-      }
       if (op == OP_SHELL) {
-        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, &LB, &stats.n_mid, &stats.n_lev,
-                            fused ? &PB : nullptr, slices))) {
-          set_empty(dst);
+        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, opf, &LB, fused ? &PB : nullptr,
+                            slices)))
           return s;
-        }
       } else {
         LB = LA;
       }
-      stats.lev_cap = std::max<uint32_t>(stats.lev_cap, std::max(LA.cap, LB.cap));
-      const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, flags};
+      lev_cap_used = std::max<uint32_t>(lev_cap_used, std::max(LA.cap, LB.cap));
+      const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, opf};
       LAUNCH(T, K_P2, launch_pass2(op, LA, LB, nx, hlo + b0, b1 - b0, src->d.z_lo, src->d.z_hi, O, st));
       CK(cudaGetLastError());
       for (LevelSlots* Lf : {&LA, &LB}) {
@@ -1147,47 +1102,79 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
         if (Lf->ovf_z) T.release(Lf->ovf_z);
       }
     }
-    unsigned hf[4];
+    // output offsets (scan of the staged counts) and the compaction into dst's current buffer
+    // (when the total fits it: the kernel checks on the device)
+    dst->n = 0;   // (from here on dst is being replaced: an error leaves it empty, run_op)
+    if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
+    if ((s = scan_counts_dev(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p))) return s;
+    if (!dst->ep.p && (s = dalloc(dst, dst->ep, sizeof(float2) * (size_t)(2 * src->n + 1024)))) return s;
+    const uint64_t ep_cap = dst->ep.bytes / sizeof(float2);
+    if (ncol > 0)
+      LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(
+                               stage, ocnt, (const uint64_t*)dst->off.p, ncol, (float2*)dst->ep.p, ep_cap, opf));
+    CK(cudaGetLastError());
+    // ---- the op's one readback
+    unsigned hf[OPF_WORDS];
+    uint64_t nout = 0;
     {
       Readback rb{src};
-      rb.add(0, flags, sizeof(hf));
+      rb.add(0, opf, sizeof(hf));
+      rb.add(sizeof(hf), (const uint64_t*)dst->off.p + ncol, sizeof(nout));
       CK(rb.wait());
       rb.get(0, hf, sizeof(hf));
+      rb.get(sizeof(hf), &nout, sizeof(nout));
     }
-    if (hf[2] == 0) break;
-    // a pass-2 union outgrew the accumulator: rerun the op with a larger one
+    const bool p1_over = hf[OPF_P1_RERUN] != 0, lv_over = hf[OPF_LV_RERUN] != 0;
+    const unsigned need = hf[OPF_P2_ACC];
+    if (!p1_over && !lv_over && need == 0) {
+      if (hf[OPF_OUT_FIT]) {   // the output outgrew dst's buffer: the exact size, compact again
+        dfree(dst, dst->ep);
+        if ((s = dalloc(dst, dst->ep, sizeof(float2) * (nout + 1)))) return s;
+        CK(cudaMemsetAsync(opf + OPF_OUT_FIT, 0, sizeof(unsigned), st));
+        if (ncol > 0)
+          LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(
+                                   stage, ocnt, (const uint64_t*)dst->off.p, ncol, (float2*)dst->ep.p, nout, opf));
+        CK(cudaGetLastError());
+      }
+      uint64_t st64[2];
+      std::memcpy(st64, hf + 8, sizeof(st64));
+      stats.n_mid = st64[0];
+      stats.n_lev = st64[1];
+      stats.n_out = nout;
+      stats.bands = (uint32_t)nb;
+      stats.p2_acc = acc;
+      stats.lev_cap = lev_cap_used;
+      dst->n = nout;
+      break;
+    }
+    // something overflowed: grow it (kept on the handle for later ops) and rerun the op.  Only the
+    // earliest stage that overflowed is trusted: later stages ran on incomplete input.
+    if (attempt >= 12) return fail(DEXEL_ECUDA, "op capacity sizing did not converge");
+    if (p1_over) {
+      int cap = src->p1_cap > 0 ? (src->p1_cap + 3) / 4 * 4 : 256;
+      while (cap < 1 << 15 && (unsigned)cap * 2 < hf[OPF_P1_LONGEST]) cap *= 2;
+      src->p1_cap = std::min(1 << 15, cap * 2);
+    }
+    if (lv_over && !p1_over) {
+      const int cap = src->lev_cap > 0 ? src->lev_cap : 8;
+      if (cap >= LV_SLOT_MAX && hf[OPF_LV_LONGEST] > (unsigned)LV_CNT_MAX)
+        return fail(DEXEL_EOVERFLOW, "a column has a level list of more than " + std::to_string(LV_CNT_MAX) +
+                                         " intervals (counted in 15 bits)");
+      src->lev_cap = std::min(LV_SLOT_MAX, 2 * cap);
+      if (cap >= LV_SLOT_MAX && attempt > 6)
+        return fail(DEXEL_EOVERFLOW, "level lists outgrow the largest slot capacity and arena");
+    }
+    if (need && !p1_over && !lv_over) {   // a pass-2 union outgrew the accumulator
+      int nacc = acc;
+      while (nacc < (int)need) nacc *= 2;
+      if (pass2_smem_bytes(op, nacc, 32) > 220 * 1024)
+        return fail(DEXEL_EOVERFLOW, "a column's pass-2 union exceeds the shared-memory accumulator (" +
+                                         std::to_string(need) + " intervals)");
+      acc = nacc;
+      src->p2_acc = acc;
+    }
     T.release(stage);
-    const int need = (int)hf[2];
-    int nacc = acc;
-    while (nacc < need) nacc *= 2;
-    if (pass2_smem_bytes(op, nacc, 32) > 220 * 1024) {
-      set_empty(dst);
-      return fail(DEXEL_EOVERFLOW, "a column's pass-2 union exceeds the shared-memory accumulator (" +
-                                       std::to_string(need) + " intervals)");
-    }
-    acc = nacc;
-    src->p2_acc = acc;
-    if (attempt > 8) return fail(DEXEL_ECUDA, "pass-2 accumulator sizing did not converge");
   }
-  stats.bands = (uint32_t)((src->nrows + band - 1) / band);
-  stats.p2_acc = acc;
-  uint64_t nout = 0;
-  dst->n = 0;   // (from here on dst is being replaced: an error leaves it empty, run_op)
-  if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
-  if ((s = scan_counts(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p, &nout))) return s;
-  {   // the output endpoints: the current buffer is reused when the size fits (dst != src)
-    const size_t need = sizeof(float2) * (nout + 1);
-    if (!(dst->ep.p && dst->ep.bytes >= need && dst->ep.bytes - need <= need / 4)) {
-      dfree(dst, dst->ep);
-      if ((s = dalloc(dst, dst->ep, need))) return s;
-    }
-  }
-  if (ncol > 0)
-    LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(
-                             stage, ocnt, (const uint64_t*)dst->off.p, ncol, (float2*)dst->ep.p));
-  CK(cudaGetLastError());
-  dst->n = nout;
-  stats.n_out = nout;
   T.prof.finish();
   if (dst->stream != st) {
     cudaEvent_t ev;
@@ -1709,7 +1696,7 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   }
   if (ncol > 0)
     LAUNCH(T, K_COMPACT, compact_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, g->stream>>>(
-                             stage, cnt, (const uint64_t*)g->off.p, ncol, (float2*)g->ep.p));
+                             stage, cnt, (const uint64_t*)g->off.p, ncol, (float2*)g->ep.p, n, flags));
   CK(cudaGetLastError());
   T.prof.finish();
   CK(timed_sync(g->stream));
@@ -1732,8 +1719,25 @@ dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offset
                {0, g->nrows, 0}, g->d.nx, g->nrows, g->d.z_lo, g->d.z_hi};
   PieceSlots P;
   uint64_t m = 0;
+  unsigned* opf = nullptr;
+  if ((s = T.get(sizeof(unsigned) * OPF_WORDS, (void**)&opf))) return s;
   // unfiltered pieces (no capsule-domination pruning): bitwise comparable with the oracle's P1
-  if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, &P, &m, nullptr))) return s;
+  for (int attempt = 0;; ++attempt) {
+    CK(cudaMemsetAsync(opf, 0, sizeof(unsigned) * OPF_WORDS, g->stream));
+    if ((s = run_pass1(g, T, rows, R, complement ? 1 : 0, 0, g->nrows, opf, &P, nullptr))) return s;
+    unsigned hf[OPF_WORDS];
+    Readback rb{g};
+    rb.add(0, opf, sizeof(hf));
+    CK(rb.wait());
+    rb.get(0, hf, sizeof(hf));
+    std::memcpy(&m, hf + 8, sizeof(m));
+    if (!hf[OPF_P1_RERUN]) break;
+    if (attempt >= 10) return fail(DEXEL_ECUDA, "pass-1 capacity sizing did not converge");
+    release_pieces(T, P);
+    int cap = g->p1_cap > 0 ? (g->p1_cap + 3) / 4 * 4 : 256;
+    while (cap < 1 << 15 && (unsigned)cap * 2 < hf[OPF_P1_LONGEST]) cap *= 2;
+    g->p1_cap = std::min(1 << 15, cap * 2);
+  }
   *n_pieces = m;
   if (cap < m) return fail(DEXEL_EOVERFLOW, "capacity < pieces");
   if (!offsets || (m && (!z || !kappa))) return fail(DEXEL_EINVAL, "NULL output buffer");
@@ -1787,6 +1791,7 @@ void dexel_destroy(dexel_grid g) {
   dfree(g, g->spare_off);
   dfree(g, g->spare_ep);
   dfree(g, g->hdr);
+  for (auto& H : g->htab) dfree(g, H.dev);
   if (g->comm) {
     cudaStreamSynchronize(g->comm);
     cudaStreamDestroy(g->comm);

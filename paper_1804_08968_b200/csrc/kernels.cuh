@@ -85,8 +85,21 @@ struct PieceSlots {
   unsigned ovf_list_cap;
   uint32_t* tile_flag; // [nrows * ntiles] a tile holds an overflow column
   uint32_t* tile_list; // tiles to rerun in list mode
-  unsigned* flags;     // [0] overflow columns, [1] longest column (when > cap), [2] tiles listed
-  unsigned long long* total;   // pieces (statistics)
+  unsigned* flags;     // [0] overflow columns, [2] tiles listed (device counters of this band/family)
+  unsigned long long* total;   // pieces (statistics, the op's counter)
+  unsigned* opf;       // the op's flag words (OpFlag): a column that does not fit asks for a rerun
+};
+
+// The op's flag words: every capacity check of an op is deferred to ONE readback at its end
+// (dexel.cu run_op_impl); a set rerun flag makes the host grow that capacity and rerun the op.
+enum OpFlag {
+  OPF_P1_RERUN = 0,    // a pass-1 column did not fit (slots + arena): grow the piece capacity
+  OPF_P1_LONGEST = 1,  // its piece count
+  OPF_LV_RERUN = 2,    // a level list did not fit (slots + arena): grow the level capacity
+  OPF_LV_LONGEST = 3,
+  OPF_P2_ACC = 4,      // a pass-2 union longer than the accumulator: its length
+  OPF_OUT_FIT = 5,     // the output did not fit dst's buffer (compaction skipped)
+  OPF_WORDS = 16,      // (+ u64 statistics from word 8: n_mid, n_lev)
 };
 
 __host__ __device__ __forceinline__ size_t chunk_index(const PieceSlots& P, int row, int q, int i) {

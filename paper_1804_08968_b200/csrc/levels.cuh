@@ -90,13 +90,13 @@ struct LvArgs {
   const float* h;          // [(R+1)^2] fl32(sqrt(r^2 - (kappa^2 + k^2) s^2)), -1 where negative
   float zlo, zhi;
   LevelSlots L;
-  unsigned* flags;         // [0] longest list seen, [1] overflow columns, [2] most pieces of one
-  unsigned long long* nlev;  // total level intervals (statistics)
+  unsigned* flags;         // [1] overflow columns (device counter of this band/family)
+  unsigned long long* nlev;  // total level intervals (statistics, the op's counter)
   unsigned long long* dbg; // diagnostics or nullptr: [0] sum of per-warp max piece counts, [1] warps
   uint32_t* ovf_list;      // main pass: columns with a list longer than cap
   unsigned ovf_list_cap;
-  const uint32_t* list;    // overflow pass: the listed columns, written to the overflow arena
-  int64_t nlist;
+  const uint32_t* list;    // overflow pass: the listed columns (count flags[1], read on the device)
+  unsigned* opf;           // the op's flag words (kernels.cuh OpFlag)
 };
 
 constexpr int LV_T = 64;
@@ -149,13 +149,21 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 6 : 8) levels_kernel(LvArgs
   __shared__ float4 ringz[LV_DC][2][LV_T];
   __shared__ uint32_t ringk[LV_DC][LV_T];
   __syncthreads();
+  // the main pass covers every column once; the overflow pass walks the listed columns (their
+  // count read on the device, no host round trip), grid-stride, whole warps together
+  const int64_t nwork = A.list ? (int64_t)min(A.ovf_list_cap, A.flags[1]) : A.ncol;
+  const int64_t gstep = A.list ? (int64_t)gridDim.x * LV_T : (int64_t)1 << 62;
+  for (int64_t gb = (int64_t)blockIdx.x * LV_T; gb < nwork; gb += gstep) {
   uint32_t tot = 0, mx = 0;
-  const int64_t g = (int64_t)blockIdx.x * LV_T + threadIdx.x;
-  const bool live = g < (A.list ? A.nlist : A.ncol);
+  const int64_t g = gb + threadIdx.x;
+  const bool live = g < nwork;
   // every lane of the warp walks the same piece index t = 0..mmax-1: the chunk reads stay
   // coalesced and the loop never diverges; a lane past its own count processes the "null
   // piece" (kappa row R+1, all NaN), which leaves the sweep unchanged
-  const int m = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
+  // (a column that outgrew its slots but found no arena slot has no pieces to read: the op is
+  // rerun with larger capacities anyway -- OPF_P1_RERUN -- so it contributes nothing now)
+  int m = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
+  if (m > A.P.cap && A.P.ovf_idx[A.list ? (int64_t)A.list[g] : g] < 0) m = 0;
   const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
   if (A.dbg && (threadIdx.x & 31) == 0) {                 // diagnostics (DEXEL_DEBUG): sum of warp maxima
     atomicAdd(A.dbg, (unsigned long long)mmax);
@@ -281,20 +289,24 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 6 : 8) levels_kernel(LvArgs
   }
   if (lost) mx = max(mx, ncap + 1);
   if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
-  if (live && mx > (unsigned)A.L.cap) {
-    atomicMax(A.flags, mx);
-    if (q < 0) {   // hand the column to the overflow pass (its arena lists hold up to m pieces)
-      atomicMax(A.flags + 2, (unsigned)m);
-      const unsigned slot = atomicAdd(A.flags + 1, 1u);
-      if (slot < A.ovf_list_cap) {
-        A.ovf_list[slot] = (uint32_t)c;
-        A.L.ovf_idx[c] = (int32_t)slot;
-      }
+  if (live && q >= 0 && mx > ncap) {      // a list outgrew even the arena: rerun the op
+    atomicOr(A.opf + OPF_LV_RERUN, 1u);
+    atomicMax(A.opf + OPF_LV_LONGEST, mx);
+  }
+  if (live && q < 0 && mx > (unsigned)A.L.cap) {   // hand the column to the overflow pass
+    const unsigned slot = atomicAdd(A.flags + 1, 1u);
+    if (slot < A.ovf_list_cap) {
+      A.ovf_list[slot] = (uint32_t)c;
+      A.L.ovf_idx[c] = (int32_t)slot;
+    } else {                              // too many long lists: rerun the op with larger slots
+      atomicOr(A.opf + OPF_LV_RERUN, 1u);
+      atomicMax(A.opf + OPF_LV_LONGEST, mx);
     }
   }
   // statistics: one atomic per warp, no block barrier (warps retire independently)
   const unsigned wsum = __reduce_add_sync(0xffffffffu, tot);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(A.nlev, (unsigned long long)wsum);
+  }
 }
 
 }  // namespace dexel

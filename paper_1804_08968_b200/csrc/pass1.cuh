@@ -141,7 +141,7 @@ __device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float
   F.pk = take ? kap : F.pk;
 }
 
-// flush the pending piece and the partial chunk; store the count; list an overflowing column
+// flush the pending piece; store the count; list an overflowing column (or ask for a rerun)
 __device__ __forceinline__ void pfam_finish(PFam& F, const PieceSlots& P, int64_t c, int jr, int tile, int ntiles,
                                             bool list_mode) {
   pfam_put(F, F.plo, F.phi, F.pk, F.has_out && F.pk != KNONE);
@@ -149,9 +149,11 @@ __device__ __forceinline__ void pfam_finish(PFam& F, const PieceSlots& P, int64_
     if (F.has_out) {
       P.cnt[c] = F.np;
       if (F.np > (uint32_t)P.cap) {                    // hand the column to list mode
-        atomicMax(P.flags + 1, F.np);
         const unsigned slot = atomicAdd(P.flags, 1u);
-        if (slot < P.ovf_list_cap) {
+        if (slot >= P.ovf_list_cap || F.np > (uint32_t)P.ovf_cap) {   // does not fit: rerun the op
+          atomicOr(P.opf + OPF_P1_RERUN, 1u);
+          atomicMax(P.opf + OPF_P1_LONGEST, F.np);
+        } else {
           P.ovf_idx[c] = (int32_t)slot;
           const size_t tf = (size_t)jr * ntiles + tile;
           if (atomicExch(P.tile_flag + tf, 1u) == 0u) {
@@ -255,10 +257,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   const int ntiles = (src.nx + 31) >> 5;
   const bool list_mode = nlist >= 0;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= (list_mode ? nlist : (int64_t)nrows_out * ntiles)) return;  // warp-uniform
   const uint32_t* tile_list = FS_ON ? PS.tile_list : PC.tile_list;
   const int32_t* ovf_idx = FS_ON ? PS.ovf_idx : PC.ovf_idx;
-  const int64_t tl = list_mode ? (int64_t)tile_list[gw] : gw + (int64_t)jr0 * ntiles;
+  // one warp's work: the output tile tl (row jr = tl / ntiles of the band, 32 columns)
+  auto process = [&](int64_t tl) {
+  __syncwarp();   // (the previous tile's reads of stage[] are done)
   const P1Tile T = p1_tile(src, row0, tl, ntiles);
   const int W = 32 + 2 * R;
   // ---- stage the window's keys: column p's list at sb[p] .. sb[p] + n - 1, then a KEY_NONE
@@ -419,6 +422,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   }
   if (FS_ON) pfam_finish(FS, PS, c, T.jr, T.tile, ntiles, list_mode);
   if (FC_ON) pfam_finish(FC, PC, c, T.jr, T.tile, ntiles, list_mode);
+  };
+  if (!list_mode) {
+    if (gw < (int64_t)nrows_out * ntiles) process(gw + (int64_t)jr0 * ntiles);   // warp-uniform
+  } else {   // the listed tiles, their count read on the device (no host round trip): grid-stride
+    const unsigned nl = min((unsigned)nlist, (FS_ON ? PS.flags : PC.flags)[2]);
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = gw; t < (int64_t)nl; t += nw) process((int64_t)tile_list[t]);
+  }
 }
 
 constexpr size_t p1s_smem() { return (size_t)P1_WARPS * (P1_STAGE + 4) * 4; }
@@ -444,12 +455,17 @@ __global__ void __launch_bounds__(P1G_T) p1g_kernel(SrcRows src, int R, int row0
   const uint32_t* tile_list = FS_ON ? PS.tile_list : PC.tile_list;
   const int32_t* ovf_idx = FS_ON ? PS.ovf_idx : PC.ovf_idx;
   const int ntiles = (src.nx + 31) >> 5;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // list mode: a thread per column of the listed tiles (32 columns each), their count read on
+  // the device, grid-stride (whole warps iterate together)
+  const int64_t nlt = list_mode ? 32 * (int64_t)min((unsigned)nlist, (FS_ON ? PS.flags : PC.flags)[2]) : 0;
+  const int64_t tstep = list_mode ? (int64_t)gridDim.x * blockDim.x : 1;   // (main mode: one pass)
+  for (int64_t t = t0; list_mode ? (t - (int64_t)(threadIdx.x & 31)) < nlt : t == t0; t += tstep) {
   // (no early return of single lanes: the statistics reduction below needs whole warps)
   int jr = 0, i = 0;
   bool live;
-  if (list_mode) {   // a thread per column of the listed tiles (32 columns each)
-    live = t < nlist * 32;
+  if (list_mode) {
+    live = t < nlt;
     if (live) {
       const int64_t tl = (int64_t)tile_list[t >> 5];
       jr = (int)(tl / ntiles);
@@ -548,6 +564,7 @@ __global__ void __launch_bounds__(P1G_T) p1g_kernel(SrcRows src, int R, int row0
   }
   if (FS_ON) pfam_finish(FS, PS, c, jr, i >> 5, ntiles, list_mode);
   if (FC_ON) pfam_finish(FC, PC, c, jr, i >> 5, ntiles, list_mode);
+  }
 }
 
 // pieces of a band (slots + arena) -> CSR (dexel_pass1, parity testing only)

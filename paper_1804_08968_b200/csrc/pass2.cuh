@@ -143,7 +143,8 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
   // loaded; returns the list length
   auto open = [&](int t, int cw, const float2*& lb, int64_t& st, P2Batch& X) -> int {
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-    const int nb = cw & LV_CNT_MAX;
+    // (a slot list longer than cap that found no arena slot: the op reruns, read what exists)
+    const int nb = (cw & LV_IN_ARENA) ? (cw & LV_CNT_MAX) : min(cw & LV_CNT_MAX, L.cap);
     if (!(cw & LV_IN_ARENA)) {
       lb = L.z + slot_z_index(L, jl, k, 1, i);
       st = (int64_t)(L.R + 2) * L.nx;   // one slot
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
     }
   }
   ocnt[c] = n;
-  if (need) atomicMax(flags + 2, need);
+  if (need) atomicMax(flags + OPF_P2_ACC, need);
 }
 
 inline size_t pass2_smem_bytes(int op, int acc, int T) {
@@ -240,11 +241,18 @@ inline size_t pass2_smem_bytes(int op, int acc, int T) {
 }
 inline int pass2_stage_cap(int op, int acc) { return op == OP_SHELL ? 2 * acc : acc + 1; }
 
-// CSR compaction: out[off[c] + t] = stage[t][c]
+// CSR compaction: out[off[c] + t] = stage[t][c] -- when the total off[ncol] fits the buffer's
+// capacity; else nothing is written and the op's OPF_OUT_FIT flag asks the host to reallocate and
+// compact again (the op's one readback tells it; the staging array is still alive then)
 __global__ void compact_kernel(const float2* __restrict__ stage, const uint32_t* __restrict__ cnt,
-                               const uint64_t* __restrict__ off, int64_t ncol, float2* __restrict__ out) {
+                               const uint64_t* __restrict__ off, int64_t ncol, float2* __restrict__ out,
+                               uint64_t cap, unsigned* __restrict__ opf) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncol) return;
+  if (off[ncol] > cap) {
+    if (c == 0) atomicOr(opf + OPF_OUT_FIT, 1u);
+    return;
+  }
   const uint32_t n = cnt[c];
   const uint64_t o = off[c];
   for (uint32_t t = 0; t < n; ++t) out[o + t] = stage[(size_t)t * ncol + c];

@@ -14,7 +14,7 @@ rows = list(csv.reader(out.splitlines()))
 hdr, units = rows[0], rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-kinds = {"p1_kernel": "pass1", "p1_dual_kernel": "pass1", "levels_kernel": "levels", "pass2s_kernel": "pass2"}
+kinds = {"p1g_kernel": "pass1", "p1s_kernel": "pass1", "levels_kernel": "levels", "pass2s_kernel": "pass2"}
 acc = {}
 for r in rows[2:]:
     name = r[ix["Kernel Name"]]
