@@ -567,44 +567,33 @@ void release_pieces(Temps& T, PieceSlots& P) {
 // h(kappa,k) = sqrt(r^2 - (kappa^2 + k^2) s^2) computed in fp64 on the host and rounded once
 // to fp32 (readings R10, R20), -1 where kappa^2 + k^2 > (r/s)^2: the device never
 // evaluates a square root of a weight, and which (kappa, k) contribute is decided exactly.
-dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, float** prune, const double** wt) {
+dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, float** prune) {
   (void)T;
   const double s = g->d.spacing;
   const int n1 = R + 1;
   const char* e = std::getenv("DEXEL_NO_PRUNE");
   const bool no_prune = e && std::atoi(e);
-  const size_t nh = (size_t)n1 * n1, nf = (nh + n1 + 1 + 1) & ~(size_t)1;   // floats, then doubles
+  const size_t nh = (size_t)n1 * n1;
   for (auto& H : g->htab)   // the same radius as a recent op: nothing to build, upload or wait for
     if (H.dev.p && H.r == r && H.s == s) {
       *out = (float*)H.dev.p;
       *prune = no_prune ? nullptr : *out + nh;
-      *wt = reinterpret_cast<const double*>(*out + nf);
       return DEXEL_OK;
     }
   dexel_grid_s::HTab& H = g->htab[g->htab_next];
   g->htab_next ^= 1;
-  // the weights W[kappa] = r^2 - kappa^2 s^2 and thresholds T[k] = k^2 s^2 in fp64; a piece at level
-  // kappa reaches level k iff W - T >= 0, and then h = sqrt(W - T), rounded once to fp32 (-1 where
-  // negative): every kernel decides reach and growth from these same numbers
-  std::vector<double> W(n1), Tk(n1);
+  std::vector<float> h(nh + n1 + 1);
   const double rr = (double)r * (double)r;
-  for (int a = 0; a < n1; ++a) {
-    W[a] = rr - (double)a * a * s * s;
-    Tk[a] = (double)a * a * s * s;
-  }
-  std::vector<float> h(nf + 4 * (size_t)n1);
   for (int a = 0; a < n1; ++a)
     for (int k = 0; k < n1; ++k) {
-      const double w = W[a] - Tk[k];
+      const double w = rr - ((double)a * a + (double)k * k) * s * s;   // exact for fp32 r, small integers
       h[(size_t)a * n1 + k] = w >= 0.0 ? (float)std::sqrt(w) : -1.0f;
     }
   // capsule-domination table for the pass-1 filter: h(kappa, 0), rounded once to fp32
   // (DEXEL_NO_PRUNE=1 disables the filter)
   // (+ one entry: the absolute part of the domination margin, 16 r 2^-24 >= 8 ulp(r), kernels.cuh)
-  for (int a = 0; a < n1; ++a) h[nh + a] = (float)std::sqrt(std::max(0.0, W[a]));
+  for (int a = 0; a < n1; ++a) h[nh + a] = (float)std::sqrt(std::max(0.0, rr - (double)a * a * s * s));
   h[nh + n1] = (float)(16.0 * (double)r * std::ldexp(1.0, -24));
-  std::memcpy(h.data() + nf, W.data(), sizeof(double) * n1);
-  std::memcpy(h.data() + nf + 2 * n1, Tk.data(), sizeof(double) * n1);
   dexel_status st;
   dfree(g, H.dev);   // (stream-ordered after the ops that used it)
   H.r = -1.f;
@@ -616,7 +605,6 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
   H.s = s;
   *out = (float*)H.dev.p;
   *prune = no_prune ? nullptr : *out + nh;
-  *wt = reinterpret_cast<const double*>(*out + nf);
   return DEXEL_OK;
 }
 
@@ -627,7 +615,7 @@ dexel_status make_htab(dexel_grid g, Temps& T, float r, int R, float** out, floa
 // larger level capacity).  (pre != nullptr: the family's pieces were computed already, by
 // run_pass1_dual)
 dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const float* htab, const float* prune,
-                        const double* wt, int complement, int lr0, int lrn, unsigned* opf, LevelSlots* L,
+                        int complement, int lr0, int lrn, unsigned* opf, LevelSlots* L,
                         const PieceSlots* pre = nullptr, bool slices = false) {
   // slices: only L_0 is needed (pass 2 reads dy = 0), so only the first chunk of levels runs
   const int nlev_compute = slices ? 1 : R + 1;
@@ -684,27 +672,8 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   };
   static const bool dbg_on = std::getenv("DEXEL_DEBUG") != nullptr;
   unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
-  LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_list_cap, nullptr, opf, wt};
-  // the z-resolution: the envelope kernel (work independent of R) or the per-level union kernel,
-  // chosen per R by measurement (DEXEL_LV_ENV=0/1 forces one)
-  static const int env_mode = [] {
-    const char* e = std::getenv("DEXEL_LV_ENV");
-    return e ? std::atoi(e) : -1;
-  }();
-  const bool use_env = !slices && R <= LVE_RMAX && (env_mode >= 0 ? env_mode == 1 : R >= LVE_RMIN);
-  if (use_env) {
-    const size_t smem = lvenv_smem(R);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-      cudaFuncSetAttribute(lvenv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
-    }
-    T.prof.pre(K_LEV);
-    if (ncol > 0) lvenv_kernel<<<(unsigned)((ncol + LVE_T - 1) / LVE_T), LVE_T, smem, g->stream>>>(A);
-    T.prof.post();
-  } else {
-    launch(A, ncol);
-  }
+  LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_list_cap, nullptr, opf};
+  launch(A, ncol);
   // the overflow pass: every listed column's lists into the arena (a fixed grid, grid-stride over
   // the count the main pass left on the device)
   LvArgs B = A;
@@ -1036,10 +1005,8 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   float* htab_b = nullptr;
   float* prune_a = nullptr;
   float* prune_b = nullptr;
-  const double* wt_a = nullptr;
-  const double* wt_b = nullptr;
-  if ((s = make_htab(src, T, r_a, Ra, &htab_a, &prune_a, &wt_a))) return s;
-  if (op == OP_SHELL && (s = make_htab(src, T, r_b, Rb, &htab_b, &prune_b, &wt_b))) return s;
+  if ((s = make_htab(src, T, r_a, Ra, &htab_a, &prune_a))) return s;
+  if (op == OP_SHELL && (s = make_htab(src, T, r_b, Rb, &htab_b, &prune_b))) return s;
   // ---- row bands: level slots of (band + R-row halo) rows, then pass 2 of the band
   const int64_t ncol = src->ncol;
   const int nx = src->d.nx;
@@ -1113,11 +1080,11 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       PieceSlots PA{}, PB{};
       if (fused && (s = run_pass1_dual(src, T, rows, Ra, lr0, lr1 - lr0, opf, &PA, &PB, prune_a, prune_b))) return s;
       // family A: S (dilate, shell r_out) or C = U \ S (erode); family B: C at r_in (shell)
-      if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, wt_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, opf, &LA,
+      if ((s = run_levels(src, T, rows, Ra, htab_a, prune_a, op == OP_ERODE ? 1 : 0, lr0, lr1 - lr0, opf, &LA,
                           fused ? &PA : nullptr, slices)))
         return s;
       if (op == OP_SHELL) {
-        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, wt_b, 1, lr0, lr1 - lr0, opf, &LB, fused ? &PB : nullptr,
+        if ((s = run_levels(src, T, rows, Rb, htab_b, prune_b, 1, lr0, lr1 - lr0, opf, &LB, fused ? &PB : nullptr,
                             slices)))
           return s;
       } else {
@@ -1286,7 +1253,6 @@ void preload_kernels(int device) {
   preload_one(levels_kernel<12>);
   preload_one(levels_kernel<14>);
   preload_one(levels_kernel<17>);
-  preload_one(lvenv_kernel);
   preload_p2<OP_DILATE>();
   preload_p2<OP_ERODE>();
   preload_p2<OP_SHELL>();

@@ -97,7 +97,6 @@ struct LvArgs {
   unsigned ovf_list_cap;
   const uint32_t* list;    // overflow pass: the listed columns (count flags[1], read on the device)
   unsigned* opf;           // the op's flag words (kernels.cuh OpFlag)
-  const double* wt;        // lvenv_kernel: W[kappa] = r^2 - kappa^2 s^2, then T[k] = k^2 s^2 (fp64, R+1 each)
 };
 
 constexpr int LV_T = 64;
@@ -178,8 +177,7 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   const float4* zc;
   const uint32_t* kc;
   int64_t cstr;
-  if (A.P.ovf_idx[c] < 0) {   // (a listed column's pieces live in the arena -- also once an envelope
-                              // pass has compacted them below cap, lvenv_kernel)
+  if (A.P.ovf_idx[c] < 0) {   // (a listed column's pieces live in the arena)
     zc = A.P.z + 2 * chunk_index(A.P, row, 0, i);
     kc = A.P.k + chunk_index(A.P, row, 0, i);
     cstr = A.P.nx;
@@ -309,267 +307,6 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   const unsigned wsum = __reduce_add_sync(0xffffffffu, tot);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(A.nlev, (unsigned long long)wsum);
   }
-}
-
-// ------------------------------------------------------------------ envelope z-resolution
-// The level sets from the column's 1D power diagram directly (App. B restricted
-// to the line z): F(z) = max_p F_p(z), F_p(z) = W_p - dist(z, [a_p, b_p])^2,
-// W_p = r^2 - kappa_p^2 s^2 (the pieces are "segment seeds" with power weight W_p), and
-// L_k = { z : F(z) >= T_k = k^2 s^2 }.
-//  * For two disjoint pieces p left of q, F_p - F_q is non-increasing in z (its derivative is
-//    F_p' - F_q' <= 0 everywhere), so the cells of the upper envelope are intervals in the pieces'
-//    order -- the half-space power diagram of the paper along one line -- and one forward stack
-//    sweep builds it (push the next piece; pop the top while the new piece wins on the top's whole
-//    cell; the boundary of two cells is where F_p = F_q, in closed form, fp64).
-//  * Within the cell of piece p, F = F_p is unimodal: rising tail, flat top W_p, falling tail.
-//    F crosses T_k upward at a_p - h(kappa_p, k) and downward at b_p + h(kappa_p, k): exactly the
-//    endpoints the per-level union computes (the same fp32 table h, the same rounding), so every
-//    level-set endpoint is emitted once, by the cell that holds it, with no per-(piece, level) work:
-//    O(pieces + level intervals) per column instead of O(pieces x (R + 1)) -- independent of r
-//    (PAPER.md:575, 581).  Which levels a cell crosses follows from F at its two boundaries
-//    (computed once per boundary and shared by both cells, so adjacent cells agree).
-//  * A cell is final once no later piece can reach its end (cells left of a_q - r): it is emitted
-//    then, so the live stack stays within reach of the sweep.  The stack lives in the column's own
-//    piece storage (pieces compacted in place: the envelope's pieces, a subset whose union of
-//    capsules equals the whole set's, which is what the arena pass reads for listed columns).
-//  * Level lists keep the layout of levels_kernel (slots, counts, overflow listing).  Adjacent
-//    components may overlap by a rounding (pass 2's union absorbs that).
-constexpr int LVE_T = 64;
-constexpr int LVE_RMIN = 8;     // envelope kernel from this R (measured)
-constexpr int LVE_RMAX = 128;   // its per-thread level counts and h table fit shared memory up to here
-
-__device__ __forceinline__ double env_f(double W, double a, double b, double z) {
-  const double d = fmax(0.0, fmax(a - z, z - b));
-  return W - d * d;
-}
-
-// the point where F_p = F_q (p left of q): F_p - F_q is non-increasing, the closed forms per region
-__device__ __forceinline__ double env_boundary(double Wp, double ap, double bp, double Wq, double aq, double bq) {
-  const double d = Wp - Wq, g = aq - bp, g2 = g * g;
-  if (d > g2) {           // p's tail reaches over q's start: against q's flat top, or both right tails
-    const double z1 = bp + sqrt(d);
-    return z1 <= bq ? z1 : 0.5 * (bp + bq) + d / (2.0 * (bq - bp));
-  }
-  if (d < -g2) {          // q's tail reaches back over p's end: against p's flat top, or both left tails
-    const double z1 = aq - sqrt(-d);
-    return z1 >= ap ? z1 : 0.5 * (ap + aq) + d / (2.0 * (aq - ap));
-  }
-  return g > 0.0 ? 0.5 * (bp + aq) + d / (2.0 * g) : bp;   // in the gap (touching, equal weights: bp)
-}
-
-__global__ void __launch_bounds__(LVE_T) lvenv_kernel(LvArgs A) {
-  extern __shared__ __align__(16) unsigned char lve_smem[];
-  const int R = A.L.R, L1 = R + 1;
-  double* Wd = reinterpret_cast<double*>(lve_smem);          // [L1]  W[kappa]
-  double* Td = Wd + L1;                                      // [L1]  T[k]
-  float* Hs = reinterpret_cast<float*>(Td + L1);              // [L1 * L1]  h(kappa, k), NaN out of reach
-  uint32_t* lc = reinterpret_cast<uint32_t*>(Hs + L1 * L1);   // [L1][LVE_T] per-level list lengths
-  for (int t = threadIdx.x; t < L1; t += LVE_T) {
-    Wd[t] = A.wt[t];
-    Td[t] = A.wt[L1 + t];
-  }
-  for (int t = threadIdx.x; t < L1 * L1; t += LVE_T) {
-    const float h = A.h[t];
-    Hs[t] = h >= 0.f ? h : __int_as_float(0x7fc00000);
-  }
-  for (int k = 0; k < L1; ++k) lc[k * LVE_T + threadIdx.x] = 0u;
-  __syncthreads();
-  const int tid = threadIdx.x;
-  const int64_t g = (int64_t)blockIdx.x * LVE_T + tid;
-  const bool live = g < A.ncol;
-  const int64_t c = live ? g : 0;
-  int m = live ? (int)A.P.cnt[c] : 0;
-  if (m > A.P.cap && A.P.ovf_idx[c] < 0) m = 0;     // (no pieces were kept: the op reruns)
-  const int row = (int)(c / A.L.nx), i = (int)(c % A.L.nx);
-  // this column's pieces (and the stack, compacted in place): element s at offset
-  // (s >> 2) * 4 * cstr + (s & 3) of zc (float2) and kc (kappa bytes)
-  float2* zc;
-  uint8_t* kc;
-  uint32_t cstr;
-  if (A.P.ovf_idx[c] < 0) {   // (slots; listed columns live in the pass-1 arena)
-    zc = reinterpret_cast<float2*>(A.P.z + 2 * chunk_index(A.P, row, 0, i));
-    kc = reinterpret_cast<uint8_t*>(A.P.k + chunk_index(A.P, row, 0, i));
-    cstr = 4u * (uint32_t)A.P.nx;
-  } else {
-    const size_t qo = (size_t)A.P.ovf_idx[c] * (A.P.ovf_cap / 4);
-    zc = reinterpret_cast<float2*>(A.P.ovf_z + 2 * qo);
-    kc = reinterpret_cast<uint8_t*>(A.P.ovf_k + qo);
-    cstr = 4u;
-  }
-  auto eoff = [&](int s) -> uint32_t { return (uint32_t)(s >> 2) * cstr + (uint32_t)(s & 3); };
-  // level lists (as levels_kernel): element e of level k at slot e + 1
-  float* Zf = reinterpret_cast<float*>(A.L.z + slot_z_index(A.L, row, 0, 0, i));
-  const uint32_t nx = (uint32_t)A.L.nx, ostep = (uint32_t)(R + 2) * nx;
-  const uint32_t cap = (uint32_t)A.L.cap;
-  const double reach = sqrt(Wd[0]);
-  uint32_t* lck = lc + tid;
-  // the level-k slot of element e, clamped to the spill cell (level R+1 of the last slot)
-  auto slot = [&](int k, uint32_t e) -> float* {
-    const uint32_t t = e + 1u;
-    const uint32_t o = t <= cap ? t * ostep + (uint32_t)k * nx : cap * ostep + (uint32_t)(R + 1) * nx;
-    return Zf + 2 * (size_t)o;
-  };
-  // the levels k with v < T_k <= top, as [k0, k1] (T_k = k^2 s^2 ascending; a first guess from
-  // sqrt, fixed up against the fp64 thresholds themselves)
-  auto krange = [&](double v, double top, int& k0, int& k1) {
-    int lo = 0;
-    if (v >= 0.0) {
-      lo = R >= 1 ? min(R + 1, (int)sqrt(v / Td[1])) : 0;
-      while (lo <= R && Td[lo] <= v) ++lo;
-      while (lo > 0 && Td[lo - 1] > v) --lo;
-    }
-    int hi = R;
-    if (!(top >= Td[R])) {
-      hi = top >= 0.0 ? (R >= 1 ? min(R, (int)sqrt(top / Td[1])) : 0) : -1;
-      while (hi < R && Td[hi + 1] <= top) ++hi;
-      while (hi >= 0 && Td[hi] > top) --hi;
-    }
-    k0 = lo;
-    k1 = hi;
-  };
-  // emit the crossings of a final cell: piece (a, b, kappa, W), cell [c0, c1), F(c0) = v0,
-  // F(c1) = v1 (-inf outside the first / last cell)
-  auto emit_cell = [&](float a, float b, int kap, double W, double c0, double c1, double v0, double v1) {
-    const float* hr = Hs + kap * L1;
-    if (c0 < (double)a) {            // rising tail: lower endpoints a - h, levels v0 < T_k <= top
-      const double top = c1 < (double)a ? v1 : W;
-      int k0, k1;
-      krange(v0, top, k0, k1);
-      for (int k = k0; k <= k1; ++k) {
-        const float h = hr[k];
-        if (!(h >= 0.f)) continue;   // (out of reach by the table: W - T_k < 0)
-        const uint32_t e = lck[k * LVE_T];
-        *slot(k, e) = a - h;
-      }
-    }
-    if (c1 > (double)b) {            // falling tail: upper endpoints b + h, levels v1 < T_k <= top
-      const double top = c0 > (double)b ? v0 : W;
-      int k0, k1;
-      krange(v1, top, k0, k1);
-      for (int k = k1; k >= k0; --k) {
-        const float h = hr[k];
-        if (!(h >= 0.f)) continue;
-        const uint32_t e = lck[k * LVE_T];
-        slot(k, e)[1] = b + h;
-        lck[k * LVE_T] = e + 1u;
-      }
-    }
-  };
-  const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
-  // the stack: elements 0 .. top of the column storage; the top and the next cell to emit in registers
-  int top = -1, ep = 0;                 // ep: the bottom-most entry not emitted yet
-  float ta = 0.f, tb = 0.f;             // the top piece
-  int tk = 0;
-  double tW = 0.0, tbeta = -INFINITY;   // its weight and cell start
-  float ea = 0.f, eb = 0.f;             // entry ep (valid while ep <= top)
-  int ek = 0;
-  double eW = 0.0, ebeta = -INFINITY, ev0 = -INFINITY;   // its cell start and F there
-  auto load = [&](int s, float& a, float& b, int& k) {
-    const uint32_t o = eoff(s);
-    const float2 v = zc[o];
-    a = v.x;
-    b = v.y;
-    k = kc[o];
-  };
-  auto store = [&](int s, float a, float b, int k) {
-    const uint32_t o = eoff(s);
-    zc[o] = make_float2(a, b);
-    kc[o] = (uint8_t)k;
-  };
-  // emit entry ep (its cell ends at c1 with F(c1) = v1 computed from it) and advance to ep + 1
-  auto emit_next = [&](double c1, double v1) {
-    emit_cell(ea, eb, ek, eW, ebeta, c1, ev0, v1);
-    ebeta = c1;
-    ev0 = v1;
-    ++ep;
-  };
-  for (int t = 0; t < mmax; ++t) {
-    if (t < m) {
-      float qa, qb;
-      int qk;
-      load(t, qa, qb, qk);
-      const double qW = Wd[qk];
-      double beta = -INFINITY;
-      // pop while the new piece wins on the top's whole cell (never below the emitted entries:
-      // those are out of its reach)
-      while (top >= 0) {
-        beta = env_boundary(tW, ta, tb, qW, qa, qb);
-        if (beta > tbeta || top < ep) break;
-        --top;
-        if (top >= 0) {
-          load(top, ta, tb, tk);
-          tW = Wd[tk];
-          if (top == 0) tbeta = -INFINITY;
-          else {
-            float pa, pb;
-            int pk;
-            load(top - 1, pa, pb, pk);
-            tbeta = env_boundary(Wd[pk], pa, pb, tW, ta, tb);
-          }
-        }
-        beta = -INFINITY;
-      }
-      ++top;
-      store(top, qa, qb, qk);
-      ta = qa; tb = qb; tk = qk; tW = qW; tbeta = beta;
-      if (ep == top) { ea = qa; eb = qb; ek = qk; eW = qW; }   // (the first entry of the live stack)
-      // cells that no later piece can reach are final: emit them
-      const double lim = (double)qa - reach;
-      while (ep < top) {
-        // the boundary of ep and ep + 1
-        double c1;
-        float na, nb;
-        int nk;
-        if (ep + 1 == top) { c1 = tbeta; na = ta; nb = tb; nk = tk; }
-        else {
-          load(ep + 1, na, nb, nk);
-          c1 = env_boundary(eW, ea, eb, Wd[nk], na, nb);
-        }
-        if (!(c1 < lim)) break;
-        emit_next(c1, env_f(eW, ea, eb, c1));
-        ea = na; eb = nb; ek = nk; eW = Wd[nk];
-      }
-    }
-  }
-  // the rest of the stack (the last cell extends to +inf)
-  while (live && ep <= top) {
-    if (ep == top) {
-      emit_next(INFINITY, -INFINITY);
-    } else {
-      float na, nb;
-      int nk;
-      load(ep + 1, na, nb, nk);
-      const double c1 = env_boundary(eW, ea, eb, Wd[nk], na, nb);
-      emit_next(c1, env_f(eW, ea, eb, c1));
-      ea = na; eb = nb; ek = nk; eW = Wd[nk];
-    }
-  }
-  // counts, statistics, overflow listing (as levels_kernel)
-  uint32_t tot = 0, mx = 0;
-  for (int k = 0; k < L1; ++k) {
-    const uint32_t n = lck[k * LVE_T];
-    if (live) A.L.cnt[slot_cnt_index(A.L, row, k, i)] = (uint16_t)min(n, (uint32_t)LV_CNT_MAX);
-    tot += n;
-    mx = max(mx, n);
-  }
-  if (live) A.P.cnt[c] = (uint32_t)(top + 1);   // the envelope's pieces (what the arena pass reads)
-  if (live && mx > cap) {
-    const unsigned sl = atomicAdd(A.flags + 1, 1u);
-    if (sl < A.ovf_list_cap) {
-      A.ovf_list[sl] = (uint32_t)c;
-      A.L.ovf_idx[c] = (int32_t)sl;
-    } else {
-      atomicOr(A.opf + OPF_LV_RERUN, 1u);
-      atomicMax(A.opf + OPF_LV_LONGEST, mx);
-    }
-  }
-  const unsigned wsum = __reduce_add_sync(0xffffffffu, live ? tot : 0u);
-  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(A.nlev, (unsigned long long)wsum);
-}
-
-inline size_t lvenv_smem(int R) {
-  const size_t L1 = (size_t)R + 1;
-  return 16 * L1 + 4 * L1 * L1 + 4 * L1 * LVE_T + 16;
 }
 
 }  // namespace dexel

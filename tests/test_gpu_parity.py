@@ -772,39 +772,3 @@ def test_error_leaves_dst_empty(dx):
     assert not off.any()
     dx.dexel_dilate(src, 3.0, dst)
     check(*dst.download(), run_oracle(host, "dilate", 3.0), what="after error")
-
-
-@pytest.mark.parametrize("env", ["1", "0"])
-def test_levels_kernels_forced(dx, env):
-    """Both z-resolution kernels on every radius range (DEXEL_LV_ENV=1: the envelope kernel, whose
-    work does not grow with R; 0: the per-level union kernel): random grids incl. non-integer r,
-    spacing != 1, thin layers, touching pieces, tiny capacities; all ops against the oracle."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import sys; sys.path.insert(0, %r)
-import numpy as np, dexelgen as G, oracle as O, paper_1804_08968_b200 as dx
-from oracle.compare import compare
-for seed in range(14):
-    rs = np.random.default_rng(5000 + seed)
-    host = G.random_grid(int(rs.integers(2, 40)), int(rs.integers(2, 30)), 6, -15.0, 15.0, seed,
-                         quantum=0.25 if seed %% 3 == 0 else None)
-    if seed %% 4 == 1:
-        host.spacing = 0.6
-    for r in (float(rs.choice([0.5, 1.0, 2.0, 3.5, 5.0, 8.0, 11.7, 16.0, 23.0, 40.0])),):
-        src = dx.Grid.from_host(host); dst = dx.Grid.like(src)
-        for op in ("dilate", "erode", "shell"):
-            if op == "shell":
-                dx.dexel_shell(src, r, r * 0.8, dst); ref = O.shell(host, r, r * 0.8)
-            else:
-                getattr(dx, "dexel_" + op)(src, r, dst); ref = getattr(O, op)(host, r)
-            off, ep = dst.download()
-            res = compare(off, ep, ref.off, ref.z, 1e-4); assert res["ok"], (seed, op, r, res)
-        src.close(); dst.close()
-print("OK")
-''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for caps in ({}, {"DEXEL_LEV_CAP": "1", "DEXEL_P1_CAP": "3"}):
-        env_ = dict(os.environ, DEXEL_LV_ENV=env, **caps)
-        out = subprocess.run([sys.executable, "-c", code], env=env_, capture_output=True, text=True, timeout=900)
-        assert out.returncode == 0 and "OK" in out.stdout, (caps, out.stdout + out.stderr)
