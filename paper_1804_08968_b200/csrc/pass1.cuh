@@ -46,7 +46,7 @@ struct PFam {
   int kap;            // its kappa (KNONE: no parent within R)
   float plo, phi;     // pending (closed, filtered-later) piece
   int pk;
-  int trow;           // threshold-table row of pk, times 32 (row 17: no pending piece)
+  uint32_t trow;      // shared address of the threshold-table row of pk (row 17: no pending piece)
   float hpk;          // H[pk] (computed-threshold mode, R > 16)
   uint32_t np;        // pieces stored
   float2* zb;         // piece 0 of this column (chunk 0)
@@ -57,6 +57,23 @@ struct PFam {
   bool has_out;
 };
 
+// shared-memory accesses through 32-bit shared addresses (computed once per kernel: a generic
+// pointer into shared memory made nvcc rebuild the window address on every sweep step)
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
 // predicated store of one piece without a branch: the (lo, hi) pair and its kappa byte
 __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo, float hi, int k, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v2.f32 [%0], {%2, %3};\n\t"
@@ -66,7 +83,7 @@ __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo,
 
 // out_kind: 0 = slots of column i of band row jr, 1 = arena slot `aslot`, 2 = no output (spill)
 __device__ __forceinline__ void pfam_init(PFam& F, const PieceSlots& P, int jr, int i, int out_kind, int aslot,
-                                          const float2* thr) {
+                                          uint32_t thr) {
   const uint32_t nc = (uint32_t)(P.cap / 4);   // chunks per column (+1: the spill chunk)
   if (out_kind == 0) {
     F.zb = reinterpret_cast<float2*>(P.z + 2 * chunk_index(P, jr, 0, i));
@@ -93,7 +110,7 @@ __device__ __forceinline__ void pfam_init(PFam& F, const PieceSlots& P, int jr, 
   F.woff = 0;
   F.plo = F.phi = 0.f;
   F.pk = KNONE;
-  F.trow = 17 * 32;
+  F.trow = thr + 17u * 32u * 8u;
   F.hpk = 0.f;
   F.zstart = 0.f;
   F.kap = KNONE;
@@ -115,7 +132,7 @@ __device__ __forceinline__ void pfam_put(PFam& F, float lo, float hi, int k, boo
 // the pending piece (table mode: thresholds from the (kp, kn) table; else from H = prune), then
 // the pending piece is stored unless dominated, and the new one becomes pending unless dominated
 template <bool TABLE, bool PRUNE>
-__device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float z, int kap, const float2* thr,
+__device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float z, int kap, uint32_t thr,
                                            const float* h0, float mabs) {
   if constexpr (!PRUNE) {
     pfam_put(F, zs, z, kap, closed);
@@ -124,7 +141,7 @@ __device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float
   bool drop_new, drop_pend;
   const bool hp = F.pk != KNONE;
   if constexpr (TABLE) {
-    const float2 th = thr[F.trow + (kap & 31)];
+    const float2 th = lds_f2(F.trow + 8u * (uint32_t)(kap & 31));
     drop_new = z - F.phi <= th.x;
     drop_pend = zs - F.plo <= th.y;
   } else {
@@ -136,7 +153,7 @@ __device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float
   const bool take = closed && !drop_new;
   F.plo = take ? zs : F.plo;
   F.phi = take ? z : F.phi;
-  if constexpr (TABLE) F.trow = take ? (kap & 31) * 32 : F.trow;
+  if constexpr (TABLE) F.trow = take ? thr + 256u * (uint32_t)(kap & 31) : F.trow;
   else F.hpk = take ? h0[kap & 255] : F.hpk;
   F.pk = take ? kap : F.pk;
 }
@@ -254,6 +271,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* stage = p1_smem + (size_t)wid * (P1_STAGE + 4);
+  const uint32_t stage_a = sh_addr(stage);
+  const uint32_t ths = sh_addr(thr_s), thc = sh_addr(thr_c);
   const int ntiles = (src.nx + 31) >> 5;
   const bool list_mode = nlist >= 0;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -299,12 +318,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       const float2* src2 = reinterpret_cast<const float2*>(ep) + cb0[q];
       for (uint32_t t = 0; t < end[q]; t += 2) {
         const float2 v = __ldg(src2 + (t >> 1));
-        stage[sb[q] + t] = fkey(v.x);
-        stage[sb[q] + t + 1] = fkey(v.y);
+        sts_u32(stage_a + 4u * (sb[q] + t), fkey(v.x));
+        sts_u32(stage_a + 4u * (sb[q] + t + 1), fkey(v.y));
       }
-      stage[sb[q] + end[q]] = KEY_NONE;
-      pos[q] = sb[q];
-      end[q] = sb[q] + end[q];
+      sts_u32(stage_a + 4u * (sb[q] + end[q]), KEY_NONE);
+      pos[q] = stage_a + 4u * sb[q];             // staged: pos is the key's shared address
+      end[q] = stage_a + 4u * (sb[q] + end[q]);
     }
   }
   __syncwarp();
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   // ep[2 cb0[q] + t]
 #pragma unroll
   for (int q = 0; q < NW; ++q)
-    nkey[q] = pos[q] < end[q] ? (staged ? stage[pos[q]] : fkey(__ldg(ep + 2 * cb0[q] + pos[q]))) : KEY_NONE;
+    nkey[q] = pos[q] < end[q] ? (staged ? lds_u32(pos[q]) : fkey(__ldg(ep + 2 * cb0[q] + pos[q]))) : KEY_NONE;
   // ---- this lane's output column and its families
   const int i = T.i0 + lane;
   const bool out_ok = i < src.nx;
@@ -324,8 +343,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       aslot = out_ok ? ovf_idx[c] : -1;
       kind = aslot >= 0 ? 1 : 2;
     }
-    if (FS_ON) pfam_init(FS, PS, T.jr, out_ok ? i : 0, kind, aslot, thr_s);
-    if (FC_ON) pfam_init(FC, PC, T.jr, out_ok ? i : 0, kind, aslot, thr_c);
+    if (FS_ON) pfam_init(FS, PS, T.jr, out_ok ? i : 0, kind, aslot, ths);
+    if (FC_ON) pfam_init(FC, PC, T.jr, out_ok ? i : 0, kind, aslot, thc);
   }
   const int pp = lane + R;
   // NW == 2: this lane's two 32-bit windows of the 64-bit mask, bits pp .. pp+31 (right) and
@@ -364,10 +383,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       for (int q = 0; q < NW; ++q) {
         const bool hit = nkey[q] == zk;
         M[q] ^= __ballot_sync(FULL, hit);
-        pos[q] += hit ? 1u : 0u;
         if constexpr (STG) {   // sentinel-terminated lists in shared memory
-          if (hit) nkey[q] = stage[pos[q]];
+          pos[q] += hit ? 4u : 0u;
+          if (hit) nkey[q] = lds_u32(pos[q]);
         } else if (hit) {
+          ++pos[q];
           nkey[q] = pos[q] < end[q] ? fkey(__ldg(ep + 2 * cb0[q] + pos[q])) : KEY_NONE;
         }
       }
@@ -391,7 +411,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
         // an event changes kappa only for lanes within R of its column: a step where no lane of
         // the warp changes (often: halo events) skips the filter / emission half (warp-uniform)
         if (!SKIP || __any_sync(FULL, chg)) {
-          pfam_close<TABLE, PRN>(FS, chg && FS.kap != KNONE, FS.zstart, z, FS.kap, thr_s, h0s, mabs_s);
+          pfam_close<TABLE, PRN>(FS, chg && FS.kap != KNONE, FS.zstart, z, FS.kap, ths, h0s, mabs_s);
           FS.kap = chg ? ks : FS.kap;
           FS.zstart = chg ? z : FS.zstart;
         }
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       if (FC_ON) {
         const bool chg = kc != FC.kap;
         if (!SKIP || __any_sync(FULL, chg)) {
-          pfam_close<TABLE, PRN>(FC, chg && FC.kap != KNONE && FC.zstart < z, FC.zstart, z, FC.kap, thr_c, h0c,
+          pfam_close<TABLE, PRN>(FC, chg && FC.kap != KNONE && FC.zstart < z, FC.zstart, z, FC.kap, thc, h0c,
                                  mabs_c);
           FC.kap = chg ? kc : FC.kap;
           FC.zstart = chg ? z : FC.zstart;
@@ -417,8 +437,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   }
   if (FC_ON) {   // C's last piece closes at z_hi
     const bool cl = FC.kap != KNONE && FC.zstart < src.zhi;
-    if (prune) pfam_close<TABLE, true>(FC, cl, FC.zstart, src.zhi, FC.kap, thr_c, h0c, mabs_c);
-    else pfam_close<TABLE, false>(FC, cl, FC.zstart, src.zhi, FC.kap, thr_c, h0c, mabs_c);
+    if (prune) pfam_close<TABLE, true>(FC, cl, FC.zstart, src.zhi, FC.kap, thc, h0c, mabs_c);
+    else pfam_close<TABLE, false>(FC, cl, FC.zstart, src.zhi, FC.kap, thc, h0c, mabs_c);
   }
   if (FS_ON) pfam_finish(FS, PS, c, T.jr, T.tile, ntiles, list_mode);
   if (FC_ON) pfam_finish(FC, PC, c, T.jr, T.tile, ntiles, list_mode);
@@ -487,8 +507,9 @@ __global__ void __launch_bounds__(P1G_T) p1g_kernel(SrcRows src, int R, int row0
   }
   live = live && kind != 2;
   PFam FS, FC;
-  if (FS_ON) pfam_init(FS, PS, jr, i, kind, aslot, thr_s);
-  if (FC_ON) pfam_init(FC, PC, jr, i, kind, aslot, thr_c);
+  const uint32_t ths = sh_addr(thr_s), thc = sh_addr(thr_c);
+  if (FS_ON) pfam_init(FS, PS, jr, i, kind, aslot, ths);
+  if (FC_ON) pfam_init(FC, PC, jr, i, kind, aslot, thc);
   if (live) {
     const uint64_t* off;
     const float* ep;
@@ -540,14 +561,14 @@ __global__ void __launch_bounds__(P1G_T) p1g_kernel(SrcRows src, int R, int row0
         if (FS_ON) {
           const int kn = kappa_of(M);
           const bool chg = kn != FS.kap;
-          pfam_close<true, PRN>(FS, chg && FS.kap != KNONE, FS.zstart, z, FS.kap, thr_s, nullptr, 0.f);
+          pfam_close<true, PRN>(FS, chg && FS.kap != KNONE, FS.zstart, z, FS.kap, ths, nullptr, 0.f);
           FS.kap = chg ? kn : FS.kap;
           FS.zstart = chg ? z : FS.zstart;
         }
         if (FC_ON) {
           const int kn = kappa_of(G & ~M);
           const bool chg = kn != FC.kap;
-          pfam_close<true, PRN>(FC, chg && FC.kap != KNONE && FC.zstart < z, FC.zstart, z, FC.kap, thr_c, nullptr,
+          pfam_close<true, PRN>(FC, chg && FC.kap != KNONE && FC.zstart < z, FC.zstart, z, FC.kap, thc, nullptr,
                                 0.f);
           FC.kap = chg ? kn : FC.kap;
           FC.zstart = chg ? z : FC.zstart;
@@ -557,9 +578,9 @@ __global__ void __launch_bounds__(P1G_T) p1g_kernel(SrcRows src, int R, int row0
     if (prune) sweep(std::true_type{});
     else sweep(std::false_type{});
     if (FC_ON)   // C's last piece closes at z_hi
-      if (prune) pfam_close<true, true>(FC, FC.kap != KNONE && FC.zstart < src.zhi, FC.zstart, src.zhi, FC.kap, thr_c,
+      if (prune) pfam_close<true, true>(FC, FC.kap != KNONE && FC.zstart < src.zhi, FC.zstart, src.zhi, FC.kap, thc,
                                         nullptr, 0.f);
-      else pfam_close<true, false>(FC, FC.kap != KNONE && FC.zstart < src.zhi, FC.zstart, src.zhi, FC.kap, thr_c,
+      else pfam_close<true, false>(FC, FC.kap != KNONE && FC.zstart < src.zhi, FC.zstart, src.zhi, FC.kap, thc,
                                    nullptr, 0.f);
   }
   if (FS_ON) pfam_finish(FS, PS, c, jr, i >> 5, ntiles, list_mode);
