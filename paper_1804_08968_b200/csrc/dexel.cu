@@ -76,6 +76,7 @@ struct dexel_grid_s {
   unsigned char* pin = nullptr;   // pinned host scratch for the small device->host readbacks
   // capacity hints carried between ops (grown on overflow)
   int lev_cap = 0, p2_acc = 0, p1_cap = 0;
+  int lev_arena = 0;   // level-list arena entries per list once lev_cap is at LV_SLOT_MAX (0: 4 lev_cap)
   // the previous input CSR after a re-upload: the next upload of a similar size fills it
   // instead of allocating (an upload must not touch the current contents until validated)
   Buf spare_off, spare_ep;
@@ -633,8 +634,9 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   L->nrows = lrn;
   L->row0 = lr0;
   L->cap = g->lev_cap > 0 ? g->lev_cap : 8;
-  // arena lists: 4x the slot capacity (at least 32); longer lists rerun the op with larger slots
-  L->ovf_cap = std::min(LV_CNT_MAX, std::max(32, 4 * L->cap));
+  // arena lists: 4x the slot capacity (at least 32); longer lists rerun the op with larger slots,
+  // then (slots at LV_SLOT_MAX) with a larger arena
+  L->ovf_cap = std::min(LV_CNT_MAX, std::max({32, 4 * L->cap, g->lev_arena}));
   const size_t nlist = (size_t)ncol * (R + 1);
   if ((s = T.get(sizeof(uint16_t) * nlist + 16, (void**)&L->cnt))) return s;
   if ((s = T.get(sizeof(int32_t) * ncol + 16, (void**)&L->ovf_idx))) return s;
@@ -645,7 +647,8 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   if ((size_t)(R + 2) * (L->cap + 1) * src.nx >= (1ull << 32))
     return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
   if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
-  if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * (R + 1) * (L->ovf_cap + 1) + 16, (void**)&L->ovf_z)))
+  if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * ((size_t)(R + 1) * (L->ovf_cap + 1) + 1) + 16,
+                 (void**)&L->ovf_z)))
     return s;
   CK(cudaMemsetAsync(flags, 0, 64, g->stream));
   CK(cudaMemsetAsync(L->ovf_idx, 0xff, sizeof(int32_t) * ncol, g->stream));   // -1: no arena slot
@@ -698,6 +701,7 @@ struct P2Out {
   float2* stage;
   uint32_t* ocnt;
   unsigned* flags;
+  float2* gacc;            // global accumulator [acc][band columns] (unions beyond shared memory) or null
 };
 
 template <int OP, int TT>
@@ -706,18 +710,23 @@ void launch_pass2_t(const LevelSlots& A, const LevelSlots& B, int nx, int row0, 
   const int acc = O.acc;
   const unsigned blocks = (unsigned)((int64_t)((nx + TT - 1) / TT) * nrows);   // (column tiles) x rows
   if (blocks == 0) return;
+  if (O.gacc) {
+    pass2s_kernel<OP, TT, true><<<blocks, TT, pass2_smem_bytes(OP, acc, TT, true), st>>>(
+        A, B, nx, row0, nrows, O.cbase, O.ncol, zlo, zhi, acc, O.stage, O.ocnt, O.flags, O.gacc);
+    return;
+  }
   const size_t smem = pass2_smem_bytes(OP, acc, TT);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(pass2s_kernel<OP, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  pass2s_kernel<OP, TT><<<blocks, TT, smem, st>>>(A, B, nx, row0, nrows, O.cbase, O.ncol, zlo, zhi, acc, O.stage,
-                                                  O.ocnt, O.flags);
+    cudaFuncSetAttribute(pass2s_kernel<OP, TT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pass2s_kernel<OP, TT, false><<<blocks, TT, smem, st>>>(A, B, nx, row0, nrows, O.cbase, O.ncol, zlo, zhi, acc,
+                                                         O.stage, O.ocnt, O.flags, nullptr);
 }
 
 // block size: 32 threads (one warp per block: measured fastest, C5 pass 2 36.6 ms at 128 threads,
 // 35.0 at 64, 34.1 at 32); the accumulators of a block always fit
 inline int pass2_block(int op, int acc) {
   int TT = 32;
-  while (TT > 32 && pass2_smem_bytes(op, acc, TT) > 220 * 1024) TT >>= 1;
+  while (TT > 32 && pass2_smem_bytes(op, acc, TT) > P2_SMEM_MAX) TT >>= 1;
   return TT;
 }
 
@@ -1071,6 +1080,11 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   for (int attempt = 0;; ++attempt) {
     const int nb = (src->nrows + band - 1) / band;
     if ((s = T.get(sizeof(float2) * (size_t)pass2_stage_cap(op, acc) * ncol + 16, (void**)&stage))) return s;
+    // unions longer than a shared-memory accumulator holds: a global one for the band's columns
+    float2* gacc = nullptr;
+    if (pass2_smem_bytes(op, acc, 32) > P2_SMEM_MAX &&
+        (s = T.get(sizeof(float2) * (size_t)acc * band * nx + 16, (void**)&gacc)))
+      return s;
     CK(cudaMemsetAsync(opf, 0, sizeof(unsigned) * OPF_WORDS, st));
     uint32_t lev_cap_used = 0;
     for (int b0 = 0; b0 < src->nrows; b0 += band) {
@@ -1091,7 +1105,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
         LB = LA;
       }
       lev_cap_used = std::max<uint32_t>(lev_cap_used, std::max(LA.cap, LB.cap));
-      const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, opf};
+      const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, opf, gacc};
       LAUNCH(T, K_P2, launch_pass2(op, LA, LB, nx, hlo + b0, b1 - b0, src->d.z_lo, src->d.z_hi, O, st));
       CK(cudaGetLastError());
       for (LevelSlots* Lf : {&LA, &LB}) {
@@ -1102,6 +1116,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
         if (Lf->ovf_z) T.release(Lf->ovf_z);
       }
     }
+    if (gacc) T.release(gacc);
     // output offsets (scan of the staged counts) and the compaction into dst's current buffer
     // (when the total fits it: the kernel checks on the device)
     dst->n = 0;   // (from here on dst is being replaced: an error leaves it empty, run_op)
@@ -1149,7 +1164,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
     }
     // something overflowed: grow it (kept on the handle for later ops) and rerun the op.  Only the
     // earliest stage that overflowed is trusted: later stages ran on incomplete input.
-    if (attempt >= 12) return fail(DEXEL_ECUDA, "op capacity sizing did not converge");
+    if (attempt >= 24) return fail(DEXEL_ECUDA, "op capacity sizing did not converge");
     if (p1_over) {
       int cap = src->p1_cap > 0 ? (src->p1_cap + 3) / 4 * 4 : 256;
       while (cap < 1 << 15 && (unsigned)cap * 2 < hf[OPF_P1_LONGEST]) cap *= 2;
@@ -1161,17 +1176,21 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
         return fail(DEXEL_EOVERFLOW, "a column has a level list of more than " + std::to_string(LV_CNT_MAX) +
                                          " intervals (counted in 15 bits)");
       src->lev_cap = std::min(LV_SLOT_MAX, 2 * cap);
-      if (cap >= LV_SLOT_MAX && attempt > 6)
-        return fail(DEXEL_EOVERFLOW, "level lists outgrow the largest slot capacity and arena");
+      if (cap >= LV_SLOT_MAX) {   // slots at their largest: grow the arena lists
+        const int ac = std::min(LV_CNT_MAX, std::max({32, 4 * cap, src->lev_arena}));
+        if (ac >= LV_CNT_MAX)
+          return fail(DEXEL_EOVERFLOW, "level lists outgrow the largest slot capacity and arena");
+        src->lev_arena = std::min(LV_CNT_MAX, std::max<int>(2 * ac, (int)std::min<unsigned>(hf[OPF_LV_LONGEST], LV_CNT_MAX)));
+      }
     }
     if (need && !p1_over && !lv_over) {   // a pass-2 union outgrew the accumulator
       int nacc = acc;
       while (nacc < (int)need) nacc *= 2;
-      if (pass2_smem_bytes(op, nacc, 32) > 220 * 1024)
-        return fail(DEXEL_EOVERFLOW, "a column's pass-2 union exceeds the shared-memory accumulator (" +
-                                         std::to_string(need) + " intervals)");
+      // (beyond P2_SMEM_MAX the accumulator moves to global memory: slower, any length)
       acc = nacc;
-      src->p2_acc = acc;
+      // (the handle keeps at most the largest shared-memory accumulator: one pathological op does
+      // not send later ops to the global one)
+      src->p2_acc = std::min(acc, (int)(P2_SMEM_MAX / (32 * sizeof(float2))) - P2_R);
     }
     T.release(stage);
   }
@@ -1232,9 +1251,10 @@ void preload_p1() {
 }
 template <int OP>
 void preload_p2() {
-  preload_one(pass2s_kernel<OP, 32>);
-  preload_one(pass2s_kernel<OP, 64>);
-  preload_one(pass2s_kernel<OP, 128>);
+  preload_one(pass2s_kernel<OP, 32, false>);
+  preload_one(pass2s_kernel<OP, 64, false>);
+  preload_one(pass2s_kernel<OP, 128, false>);
+  preload_one(pass2s_kernel<OP, 32, true>);
 }
 void preload_kernels(int device) {
   static bool done[64] = {false};
@@ -1545,12 +1565,14 @@ dexel_status compose(int op1, int op2, dexel_grid src, float r, dexel_grid dst) 
   dexel_status s = dexel_create(&d, &tmp);
   if (s) return s;
   tmp->lev_cap = src->lev_cap;
+  tmp->lev_arena = src->lev_arena;
   tmp->p1_cap = src->p1_cap;
   tmp->p2_acc = src->p2_acc;
   s = run_op(op1, src, r, r, tmp);
   if (!s) {
     s = run_op(op2, tmp, r, r, dst);
     src->lev_cap = std::max(src->lev_cap, tmp->lev_cap);
+    src->lev_arena = std::max(src->lev_arena, tmp->lev_arena);
     src->p1_cap = std::max(src->p1_cap, tmp->p1_cap);
     src->p2_acc = std::max(src->p2_acc, tmp->p2_acc);
   }

@@ -128,6 +128,28 @@ __device__ __forceinline__ bool dom_margin(float lhs, float rhs, float mabs) {
   return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs)) - mabs;
 }
 
+// shared-memory accesses through 32-bit shared addresses (computed once per kernel: a generic
+// pointer into shared memory made nvcc rebuild the window address on every sweep step)
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
 // capsule-domination thresholds of every (pending kappa, new kappa) pair (pass1.cuh, R <= 16)
 __device__ __forceinline__ void p1_thr_init(float2* thr, const float* __restrict__ prune, int R) {
   const float mabs = prune[R + 1];   // absolute part of the margin (16 r 2^-24, see above)

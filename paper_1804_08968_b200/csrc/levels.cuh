@@ -61,7 +61,8 @@ struct LevelSlots {
   int ry;            // row offsets pass 2 reads: |dy| <= ry (R; 0 for slices, 2D offsets of each row)
   int row0;          // row (in the op's extended-row numbering) of slot row 0
   // columns with a list longer than cap keep all their lists in the overflow arena:
-  // list k of overflow slot q at ovf_z[(q*(R+1) + k)*(ovf_cap+1) + t], t = 1..ovf_cap (0 dummy);
+  // list k of overflow slot q at ovf_z[q*((R+1)*(ovf_cap+1) + 1) + k*(ovf_cap+1) + t], t = 1..ovf_cap
+  // (0 dummy; the one extra entry per slot is its spill cell);
   // ovf_cap = the most pieces of any listed column (a level list never holds more components
   // than the column has pieces: each push starts with one)
   int32_t* ovf_idx;  // [nrows*nx] overflow slot of a column (valid only where some count > cap)
@@ -81,7 +82,7 @@ __host__ __device__ __forceinline__ size_t slot_z_index(const LevelSlots& L, int
 }
 
 __host__ __device__ __forceinline__ size_t ovf_z_index(const LevelSlots& L, int q, int k, int t) {
-  return ((size_t)q * (L.R + 1) + k) * (size_t)(L.ovf_cap + 1) + t;
+  return (size_t)q * ((size_t)(L.R + 1) * (L.ovf_cap + 1) + 1) + (size_t)k * (L.ovf_cap + 1) + t;
 }
 
 struct LvArgs {
@@ -102,11 +103,11 @@ struct LvArgs {
 constexpr int LV_T = 64;
 constexpr int LV_DC = 3;     // piece chunks (4 pieces each) per thread in the cp.async ring
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {   // dst: shared address
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -194,8 +195,9 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   const uint32_t ostep = q < 0 ? (uint32_t)(R + 2) * nx : 1u;           // one slot
   const uint32_t olev = q < 0 ? nx : (uint32_t)(A.L.ovf_cap + 1);      // one level
   const uint32_t ncap = q < 0 ? (uint32_t)A.L.cap : (uint32_t)A.L.ovf_cap;
-  // the spill cell: level R+1 of the last slot (main pass), the last arena entry (overflow pass)
-  const uint32_t olim = q < 0 ? ncap * ostep + (uint32_t)(R + 1 - k0) * nx : (uint32_t)(R + 1 - k0) * olev - 1u;
+  // the spill cell: level R+1 of the last slot (main pass), the arena slot's extra entry (overflow
+  // pass) -- never a list entry, so an offset that reaches it has saturated (the list overflowed)
+  const uint32_t olim = q < 0 ? ncap * ostep + (uint32_t)(R + 1 - k0) * nx : (uint32_t)(R + 1 - k0) * olev;
   float cs[LMAX], ce[LMAX], pce[LMAX];
   uint32_t o[LMAX];
   bool lost = false;   // a popped component had been pushed beyond the capacity (column overflows)
@@ -204,41 +206,44 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     cs[k] = INFINITY;     // empty top
     ce[k] = -INFINITY;
     pce[k] = -INFINITY;   // no previous component
-    o[k] = (uint32_t)k * olev;
+    o[k] = min((uint32_t)k * olev, olim);
   }
   const int nchunk = (m + 3) >> 2;
+  // shared addresses computed once (ring slots of this thread, the h table)
+  const uint32_t rz_a = sh_addr(&ringz[0][0][threadIdx.x]), rk_a = sh_addr(&ringk[0][threadIdx.x]);
+  const uint32_t hs_a = sh_addr(Hs);
   auto issue = [&](int cq) {
     if (cq < nchunk) {
-      const int u = cq % LV_DC;
+      const uint32_t u = (uint32_t)(cq % LV_DC);
       const float4* src = zc + 2 * (int64_t)cq * cstr;
-      cp_async16(&ringz[u][0][threadIdx.x], src);
-      cp_async16(&ringz[u][1][threadIdx.x], src + 1);
-      cp_async4(&ringk[u][threadIdx.x], kc + (int64_t)cq * cstr);
+      cp_async16(rz_a + u * (2 * LV_T * 16), src);
+      cp_async16(rz_a + u * (2 * LV_T * 16) + LV_T * 16, src + 1);
+      cp_async4(rk_a + u * (LV_T * 4), kc + (int64_t)cq * cstr);
     }
     cp_async_commit();   // (empty groups too: the wait count stays uniform)
   };
 #pragma unroll
   for (int t = 0; t < LV_DC - 1; ++t) issue(t);
   uint32_t kw = 0;
+  uint32_t u = 0;                     // ring slot of chunk t / 4
   for (int t = 0; t < mmax; ++t) {
-    const int u = (t >> 2) % LV_DC;
     if ((t & 3) == 0) {
       issue((t >> 2) + LV_DC - 1);
       cp_async_wait<LV_DC - 1>();     // chunk t/4 has landed (this thread's own copies)
-      kw = ringk[u][threadIdx.x];
+      kw = lds_u32(rk_a + u * (LV_T * 4));
     }
     float2 p = make_float2(0.f, 0.f);
     int nk = L1;                      // past the column's pieces: the null piece
     if (t < m) {
-      const float2* half = reinterpret_cast<const float2*>(&ringz[u][(t >> 1) & 1][threadIdx.x]);
-      p = half[t & 1];
+      p = lds_f2(rz_a + u * (2 * LV_T * 16) + (uint32_t)((t >> 1) & 1) * (LV_T * 16) + (uint32_t)(t & 1) * 8u);
       nk = (int)((kw >> (8u * (uint32_t)(t & 3))) & 0xffu);
     }
-    const float4* hrow = reinterpret_cast<const float4*>(Hs + nk * HS);
+    if ((t & 3) == 3) u = u == LV_DC - 1 ? 0u : u + 1u;
+    const uint32_t hrow = hs_a + (uint32_t)(nk * HS) * 4u;
     float hv[4 * NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const float4 v = hrow[j];
+      const float4 v = lds_f4(hrow + 16u * j);
       hv[4 * j] = v.x; hv[4 * j + 1] = v.y; hv[4 * j + 2] = v.z; hv[4 * j + 3] = v.w;
     }
     // reach is monotone in k: skip when no lane's piece reaches this chunk (warp-uniform).
@@ -251,9 +256,10 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
       const float s = p.x - hv[k], e = p.y + hv[k];
       const bool push = s > ce[k];
       // push: the top is written to its slot (the first push writes the empty top into the
-      // dummy slot 0), predicated without a branch, the offset clamped into the spill cell
-      st_pred_f2(Zd + min(o[k], olim), cs[k], ce[k], push);
-      o[k] += push ? ostep : 0u;
+      // dummy slot 0), predicated without a branch; the offset saturates at the spill cell
+      // (one VIADDMNMX: a column that reaches it has overflowed and is redone in the arena)
+      st_pred_f2(Zd + o[k], cs[k], ce[k], push);
+      o[k] = push ? min(o[k] + ostep, olim) : o[k];
       pce[k] = push ? ce[k] : pce[k];
       cs[k] = push ? s : fminf(cs[k], s);
       ce[k] = push ? e : fmaxf(ce[k], e);
@@ -264,13 +270,17 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
 #pragma unroll
       for (int k = 0; k < LMAX; ++k) {
         while (cs[k] <= pce[k]) {
+          if (o[k] == olim) {            // saturated: the stack's top entries were lost
+            lost = true;
+            pce[k] = -INFINITY;
+            break;
+          }
           const uint32_t j = o[k] - ostep;                      // the previous component's slot
-          lost |= (j - (uint32_t)k * olev) / ostep > ncap;      // it went to the spill cell
-          const float2 pv = Zd[min(j, olim)];
+          const float2 pv = Zd[j];
           cs[k] = fminf(cs[k], pv.x);
           o[k] = j;
           // the new previous component (the dummy slot 0 ends the stack: pce = -inf)
-          pce[k] = j - (uint32_t)k * olev > ostep ? Zd[min(j - ostep, olim)].y : -INFINITY;
+          pce[k] = j - (uint32_t)k * olev > ostep ? Zd[j - ostep].y : -INFINITY;
         }
       }
     }
@@ -278,7 +288,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
 #pragma unroll
   for (int k = 0; k < LMAX; ++k) {
     const bool top = cs[k] < ce[k];   // (the top is empty only if no piece reached this level)
-    st_pred_f2(Zd + min(o[k], olim), cs[k], ce[k], top);
+    st_pred_f2(Zd + o[k], cs[k], ce[k], top);
+    lost |= k0 + k <= R && o[k] == olim;   // the offset saturated: the count is lost
     const uint32_t nk_ = top ? (o[k] - (uint32_t)k * olev) / ostep : 0u;   // slots 1..n
     if (live && k0 + k <= R) {
       A.L.cnt[slot_cnt_index(A.L, row, k0 + k, i)] =

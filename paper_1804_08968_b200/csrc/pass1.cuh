@@ -57,23 +57,6 @@ struct PFam {
   bool has_out;
 };
 
-// shared-memory accesses through 32-bit shared addresses (computed once per kernel: a generic
-// pointer into shared memory made nvcc rebuild the window address on every sweep step)
-__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ float2 lds_f2(uint32_t a) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-  return v;
-}
-
 // predicated store of one piece without a branch: the (lo, hi) pair and its kappa byte
 __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo, float hi, int k, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v2.f32 [%0], {%2, %3};\n\t"

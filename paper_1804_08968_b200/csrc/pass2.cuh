@@ -33,7 +33,8 @@ enum { OP_DILATE = 0, OP_ERODE = 1, OP_SHELL = 2 };
 // element that reaches outside merges the overlapped run of intervals and shifts the tail.
 // Returns the new count (> cap: overflow, contents truncated).
 struct Acc {
-  float2* v;   // v[t * T]
+  float2* v;   // v[t * s]: shared memory (s = T, a compile-time constant) or global (the band's columns)
+  int64_t s;
   int n;
 };
 
@@ -43,19 +44,19 @@ __device__ __forceinline__ void acc_insert(Acc& A, int& p, float2& w, float a, f
   // w caches v[p] (valid while p < n), so an element covered at the cursor costs no load
   while (p < A.n && w.y < a) {
     ++p;
-    if (p < A.n) w = A.v[p * T];
+    if (p < A.n) w = A.v[p * A.s];
   }
   if (p < A.n) {
     if (w.x <= a && b <= w.y) return;                 // covered
     if (w.x <= b) {                                   // overlaps [w.x, w.y]: merge the run p..q
       int q = p;
       float e = fmaxf(b, w.y);
-      while (q + 1 < A.n && A.v[(q + 1) * T].x <= e) { ++q; e = fmaxf(e, A.v[q * T].y); }
+      while (q + 1 < A.n && A.v[(q + 1) * A.s].x <= e) { ++q; e = fmaxf(e, A.v[q * A.s].y); }
       w = make_float2(fminf(a, w.x), e);
-      A.v[p * T] = w;
+      A.v[p * A.s] = w;
       const int drop = q - p;
       if (drop) {
-        for (int t = q + 1; t < A.n; ++t) A.v[(t - drop) * T] = A.v[t * T];
+        for (int t = q + 1; t < A.n; ++t) A.v[(t - drop) * A.s] = A.v[t * A.s];
         A.n -= drop;
       }
       return;
@@ -63,9 +64,9 @@ __device__ __forceinline__ void acc_insert(Acc& A, int& p, float2& w, float a, f
   }
   // disjoint from everything: insert before p (shift the tail right)
   if (A.n >= cap) { *need = max(*need, (unsigned)(A.n + 1)); return; }
-  for (int t = A.n; t > p; --t) A.v[t * T] = A.v[(t - 1) * T];
+  for (int t = A.n; t > p; --t) A.v[t * A.s] = A.v[(t - 1) * A.s];
   w = make_float2(a, b);
-  A.v[p * T] = w;
+  A.v[p * A.s] = w;
   ++A.n;
 }
 
@@ -176,11 +177,13 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
 // output rows [row0, row0 + nrows_out) (extended-row numbering of the level slots) of a band;
 // output column c_local of the band is global output column cbase + c_local; the staging
 // array is [t][ncol_total]
-template <int OP, int T>
+// GACC: the accumulator lives in global memory ([acc][band columns], gacc) -- for unions longer
+// than the shared memory holds; else in shared memory
+template <int OP, int T, bool GACC>
 __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelSlots B, int nx, int row0, int nrows_out,
                                                    int64_t cbase, int64_t ncol, float zlo, float zhi, int acc,
                                                    float2* __restrict__ ostage, uint32_t* __restrict__ ocnt,
-                                                   unsigned* flags) {
+                                                   unsigned* flags, float2* __restrict__ gacc) {
   extern __shared__ __align__(16) float2 p2_smem[];
   const int tid = threadIdx.x;
   // column-tile-major block order: consecutive blocks are consecutive rows of one tile of T
@@ -193,17 +196,17 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
   const int64_t c = cbase + cl;
   const int jg = row0 + jr;
   unsigned need = 0;
-  Acc U{p2_smem + tid, 0};
-  float2* scratch = p2_smem + (size_t)acc * T + tid;     // [P2_R][T]
+  Acc U = GACC ? Acc{gacc + cl, (int64_t)nrows_out * nx, 0} : Acc{p2_smem + tid, T, 0};
+  float2* scratch = p2_smem + (GACC ? 0 : (size_t)acc * T) + tid;     // [P2_R][T]
   p2_family<T>(A, i, jg, zlo, zhi, U, scratch, acc, &need);
   uint32_t n = 0;
   if (OP == OP_DILATE) {
-    for (int t = 0; t < U.n; ++t) ostage[(size_t)t * ncol + c] = U.v[t * T];
+    for (int t = 0; t < U.n; ++t) ostage[(size_t)t * ncol + c] = U.v[t * U.s];
     n = U.n;
   } else if (OP == OP_ERODE) {
     float cur = zlo;
     for (int t = 0; t < U.n; ++t) {
-      const float2 v = U.v[t * T];
+      const float2 v = U.v[t * U.s];
       if (v.x > cur) ostage[(size_t)(n++) * ncol + c] = make_float2(cur, v.x);
       cur = v.y;
     }
@@ -213,15 +216,15 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
     // shared accumulator for D_rin(C), then intersect into the lower half (the result has
     // at most |U| + |V| - 1 <= 2 acc - 1 intervals and is written behind the reads)
     const int nu = U.n;
-    for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * T];
+    for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * U.s];
     // D_rin(C) only matters inside D_rout(S): an empty D(S) skips it, and its list elements are
     // clipped to D(S)'s hull instead of [z_lo, z_hi] (fewer insertions, a shorter accumulator)
-    if (nu > 0) p2_family<T>(B, i, jg, U.v[0].x, U.v[(nu - 1) * T].y, U, scratch, acc, &need);
+    if (nu > 0) p2_family<T>(B, i, jg, U.v[0].x, U.v[(nu - 1) * U.s].y, U, scratch, acc, &need);
     else U.n = 0;
     int p = 0, q = 0;
     float2 u = nu > 0 ? ostage[(size_t)acc * ncol + c] : make_float2(0.f, 0.f);
     while (p < nu && q < U.n) {
-      const float2 v = U.v[q * T];
+      const float2 v = U.v[q * U.s];
       const float lo = fmaxf(u.x, v.x), hi = fminf(u.y, v.y);
       if (lo < hi) ostage[(size_t)(n++) * ncol + c] = make_float2(lo, hi);
       if (u.y < v.y) {
@@ -235,10 +238,11 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
   if (need) atomicMax(flags + OPF_P2_ACC, need);
 }
 
-inline size_t pass2_smem_bytes(int op, int acc, int T) {
+inline size_t pass2_smem_bytes(int op, int acc, int T, bool gacc = false) {
   (void)op;
-  return (size_t)(acc + P2_R) * T * sizeof(float2);
+  return (size_t)((gacc ? 0 : acc) + P2_R) * T * sizeof(float2);
 }
+constexpr size_t P2_SMEM_MAX = 220 * 1024;   // shared memory an accumulator block may take
 inline int pass2_stage_cap(int op, int acc) { return op == OP_SHELL ? 2 * acc : acc + 1; }
 
 // CSR compaction: out[off[c] + t] = stage[t][c] -- when the total off[ncol] fits the buffer's

@@ -736,6 +736,19 @@ def test_many_layer_column(dx, op):
         check(off, ep, run_oracle(host, op, r), what=f"300 layers {op} r={r}")
 
 
+@pytest.mark.parametrize("op", ["dilate", "shell"])
+def test_level_list_beyond_arena(dx, op):
+    """1500 thin layers: level lists longer than the largest slot capacity (255) and its default
+    arena (4 x 255 entries) saturate their offsets, the op reruns with a doubled arena until they
+    fit (levels.cuh spill cell), and the result matches the oracle."""
+    col = [(float(t) * 0.25 - 200.0, float(t) * 0.25 - 199.9) for t in range(1500)]
+    cols = [col if (i + j) % 2 == 0 else col[::5] for j in range(3) for i in range(4)]
+    host = _grid(4, 3, cols, -201.0, 201.0)
+    for r in (0.05, 1.3):
+        off, ep, _ = run_gpu(dx, host, op, r)
+        check(off, ep, run_oracle(host, op, r), what=f"1500 layers {op} r={r}")
+
+
 def test_caller_stream(dx):
     """A handle on a caller-supplied stream (torch side stream): ops run on it, results match the
     oracle, and work queued on the stream before the op is ordered before it."""
