@@ -626,7 +626,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   else if ((s = run_pass1(g, T, src, R, complement, lr0, lrn, opf, &P, prune))) return s;
   const int64_t ncol = (int64_t)lrn * src.nx;
   unsigned* flags = nullptr;
-  if ((s = T.get(64, (void**)&flags))) return s;
+  if ((s = T.get(128, (void**)&flags))) return s;
   unsigned long long* nlev = reinterpret_cast<unsigned long long*>(opf + 10);
   L->R = R;
   L->ry = slices ? 0 : R;
@@ -650,7 +650,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * ((size_t)(R + 1) * (L->ovf_cap + 1) + 1) + 16,
                  (void**)&L->ovf_z)))
     return s;
-  CK(cudaMemsetAsync(flags, 0, 64, g->stream));
+  CK(cudaMemsetAsync(flags, 0, 128, g->stream));
   CK(cudaMemsetAsync(L->ovf_idx, 0xff, sizeof(int32_t) * ncol, g->stream));   // -1: no arena slot
   // levels per thread: the smallest instantiated chunk size covering R+1 in as few chunks of
   // <= max_chunk (larger chunks cost more in registers/occupancy than they save)
@@ -677,6 +677,15 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   unsigned long long* dbg = dbg_on ? (unsigned long long*)(flags + 12) : nullptr;
   LvArgs A{P, ncol, htab, src.zlo, src.zhi, *L, flags, nlev, dbg, ovf_list, ovf_list_cap, nullptr, opf};
   launch(A, ncol);
+  if (dbg) {   // (diagnostics only: waits)
+    unsigned long long hd[3];
+    CK(cudaMemcpyAsync(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    std::fprintf(stderr, "[dexel] levels rows %d..%d main pass: %lld columns, %.2f pieces per column, "
+                 "%.2f per lane (warp maxima)\n", lr0, lr0 + lrn, (long long)ncol,
+                 (double)hd[2] / std::max<int64_t>(1, ncol), (double)hd[0] / std::max(1ull, hd[1]));
+    CK(cudaMemsetAsync(dbg, 0, sizeof(hd), g->stream));
+  }
   // the overflow pass: every listed column's lists into the arena (a fixed grid, grid-stride over
   // the count the main pass left on the device)
   LvArgs B = A;
@@ -684,10 +693,11 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   launch(B, std::min<int64_t>(ovf_list_cap, 148 * 8 * LV_T));
   CK(cudaGetLastError());
   if (dbg) {   // (diagnostics only: waits)
-    unsigned long long hd[2];
-    CK(cudaMemcpy(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost));
-    std::fprintf(stderr, "[dexel] levels rows %d..%d: %lld columns, warps %llu, mean warp max %.1f pieces\n",
-                 lr0, lr0 + lrn, (long long)ncol, hd[1], (double)hd[0] / std::max(1ull, hd[1]));
+    unsigned long long hd[3];
+    CK(cudaMemcpyAsync(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    std::fprintf(stderr, "[dexel] levels rows %d..%d overflow pass: %llu warps, %.1f pieces per lane\n",
+                 lr0, lr0 + lrn, hd[1], (double)hd[0] / std::max(1ull, hd[1]));
   }
   release_pieces(T, P);
   T.release(ovf_list);

@@ -93,7 +93,7 @@ struct LvArgs {
   LevelSlots L;
   unsigned* flags;         // [1] overflow columns (device counter of this band/family)
   unsigned long long* nlev;  // total level intervals (statistics, the op's counter)
-  unsigned long long* dbg; // diagnostics or nullptr: [0] sum of per-warp max piece counts, [1] warps
+  unsigned long long* dbg; // diagnostics or nullptr: [0] sum of per-warp max piece counts, [1] warps, [2] pieces
   uint32_t* ovf_list;      // main pass: columns with a list longer than cap
   unsigned ovf_list_cap;
   const uint32_t* list;    // overflow pass: the listed columns (count flags[1], read on the device)
@@ -166,9 +166,13 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   int m = live ? (int)A.P.cnt[A.list ? (int64_t)A.list[g] : g] : 0;
   if (m > A.P.cap && A.P.ovf_idx[A.list ? (int64_t)A.list[g] : g] < 0) m = 0;
   const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
-  if (A.dbg && (threadIdx.x & 31) == 0) {                 // diagnostics (DEXEL_DEBUG): sum of warp maxima
-    atomicAdd(A.dbg, (unsigned long long)mmax);
-    atomicAdd(A.dbg + 1, 1ull);
+  if (A.dbg) {                 // diagnostics (DEXEL_DEBUG): sums of warp maxima and of counts, warps
+    const unsigned msum = __reduce_add_sync(0xffffffffu, (unsigned)m);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(A.dbg, (unsigned long long)mmax);
+      atomicAdd(A.dbg + 1, 1ull);
+      atomicAdd(A.dbg + 2, (unsigned long long)msum);
+    }
   }
   const int64_t c = live ? (A.list ? (int64_t)A.list[g] : g) : 0;
   const int q = A.list ? (int)g : -1;
