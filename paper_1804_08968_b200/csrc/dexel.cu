@@ -633,7 +633,9 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   L->nx = src.nx;
   L->nrows = lrn;
   L->row0 = lr0;
-  L->cap = g->lev_cap > 0 ? g->lev_cap : 8;
+  // slots per list: the level capacity + the LV_CLAMP - 1 slots a list may run past its clamp point
+  // between two clamps (levels.cuh)
+  L->cap = (g->lev_cap > 0 ? g->lev_cap : 8) + LV_CLAMP - 1;
   // arena lists: 4x the slot capacity (at least 32); longer lists rerun the op with larger slots,
   // then (slots at LV_SLOT_MAX) with a larger arena
   L->ovf_cap = std::min(LV_CNT_MAX, std::max({32, 4 * L->cap, g->lev_arena}));
@@ -647,7 +649,7 @@ dexel_status run_levels(dexel_grid g, Temps& T, const SrcRows& src, int R, const
   if ((size_t)(R + 2) * (L->cap + 1) * src.nx >= (1ull << 32))
     return fail(DEXEL_EOVERFLOW, "level slot offsets exceed 32 bits (grid too wide for this radius)");
   if ((s = T.get(sizeof(float2) * nslot + 16, (void**)&L->z))) return s;
-  if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * ((size_t)(R + 1) * (L->ovf_cap + 1) + 1) + 16,
+  if ((s = T.get(sizeof(float2) * (size_t)ovf_list_cap * ((size_t)(R + 1) * (L->ovf_cap + 1) + LV_CLAMP) + 16,
                  (void**)&L->ovf_z)))
     return s;
   CK(cudaMemsetAsync(flags, 0, 128, g->stream));
@@ -1041,7 +1043,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   size_t row_bytes = (size_t)nx * ((size_t)(pcap / 4 + 1) * 36 + 8) * (fused ? 2 : 1);
   for (int f = 0; f < nfam; ++f) {
     const int Rf = f == 0 ? Ra : Rb;
-    row_bytes += (size_t)nx * ((Rf + 1) * sizeof(uint16_t) + (Rf + 2) * sizeof(float2) * (size_t)(lcap + 1));
+    row_bytes += (size_t)nx * ((Rf + 1) * sizeof(uint16_t) + (Rf + 2) * sizeof(float2) * (size_t)(lcap + LV_CLAMP));
   }
   // slots of one band (pieces + level sets, all families): fewer, taller bands recompute fewer
   // halo rows (2R per band); the budget leaves room for the output staging and the caller
@@ -1114,7 +1116,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       } else {
         LB = LA;
       }
-      lev_cap_used = std::max<uint32_t>(lev_cap_used, std::max(LA.cap, LB.cap));
+      lev_cap_used = std::max<uint32_t>(lev_cap_used, std::max(LA.cap, LB.cap) - (LV_CLAMP - 1));
       const P2Out O{(int64_t)b0 * nx, ncol, acc, stage, ocnt, opf, gacc};
       LAUNCH(T, K_P2, launch_pass2(op, LA, LB, nx, hlo + b0, b1 - b0, src->d.z_lo, src->d.z_hi, O, st));
       CK(cudaGetLastError());

@@ -88,6 +88,7 @@ struct PieceSlots {
   unsigned* flags;     // [0] overflow columns, [2] tiles listed (device counters of this band/family)
   unsigned long long* total;   // pieces (statistics, the op's counter)
   unsigned* opf;       // the op's flag words (OpFlag): a column that does not fit asks for a rerun
+  uint32_t one = 1;    // 1, opaque to the compiler (fsel: zero = one - 1, padd)
 };
 
 // The op's flag words: every capacity check of an op is deferred to ONE readback at its end
@@ -126,6 +127,29 @@ __host__ __device__ __forceinline__ size_t chunk_index(const PieceSlots& P, int 
 // DEXEL_NO_PRUNE=1).  Rounding can keep a dominated piece, never drop a needed one.
 __device__ __forceinline__ bool dom_margin(float lhs, float rhs, float mabs) {
   return lhs <= rhs - 1e-6f * (1.0f + fabsf(rhs)) - mabs;
+}
+
+// Selects and conditional adds that issue on the FMA pipe.  The sweeps are ALU-pipe-bound (compares,
+// min/max, bit ops and the selects ptxas makes of every ?: and predicated move all go to the ALU
+// pipe, the FMA pipe idles at half the rate): a predicated multiply-add by a 0 / 1 the compiler
+// cannot see through (derived from a kernel argument) is a move / add on the FMA pipe.
+__device__ __forceinline__ uint32_t fsel(bool p, uint32_t a, uint32_t b, uint32_t zero) {   // p ? a : b
+  // b = b * zero + a under p (zero: an opaque 0): the product involves b, so ptxas cannot share it
+  // between two selects of the same value (it would compute a once and select on the ALU)
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q mad.lo.u32 %0, %0, %3, %2;\n\t}"
+      : "+r"(b) : "r"((uint32_t)p), "r"(a), "r"(zero));
+  return b;
+}
+__device__ __forceinline__ int fsel(bool p, int a, int b, uint32_t zero) {
+  return (int)fsel(p, (uint32_t)a, (uint32_t)b, zero);
+}
+__device__ __forceinline__ float fsel(bool p, float a, float b, uint32_t zero) {
+  return __uint_as_float(fsel(p, __float_as_uint(a), __float_as_uint(b), zero));
+}
+__device__ __forceinline__ uint32_t padd(bool p, uint32_t x, uint32_t d, uint32_t one) {   // p ? x + d : x
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q mad.lo.u32 %0, %2, %3, %0;\n\t}"
+      : "+r"(x) : "r"((uint32_t)p), "r"(d), "r"(one));
+  return x;
 }
 
 // shared-memory accesses through 32-bit shared addresses (computed once per kernel: a generic

@@ -53,6 +53,11 @@ namespace dexel {
 constexpr int LV_SLOT_MAX = 255;    // largest slot capacity the host grows to (then: the arena)
 constexpr int LV_CNT_MAX = 0x7fff;  // longest list a u16 count (bit 15 = arena flag) can describe
 constexpr uint16_t LV_IN_ARENA = 0x8000;   // count flag: the column's lists live in the overflow arena
+// the level sweep clamps its slot offsets once per LV_CLAMP pieces (not per piece): a list may run
+// LV_CLAMP - 1 slots past the clamp point before the next clamp, so the last LV_CLAMP - 1 slots of a
+// row (spill level R+1) and LV_CLAMP spill entries per arena slot absorb those writes, and a list is
+// complete only if it ends LV_CLAMP - 1 slots short of the capacity (slot capacity >= LV_CLAMP)
+constexpr int LV_CLAMP = 4;
 
 struct LevelSlots {
   uint16_t* cnt;     // [nrows][R+1][nx]  list lengths (<= LV_CNT_MAX); LV_IN_ARENA set: the list is in the arena
@@ -61,8 +66,8 @@ struct LevelSlots {
   int ry;            // row offsets pass 2 reads: |dy| <= ry (R; 0 for slices, 2D offsets of each row)
   int row0;          // row (in the op's extended-row numbering) of slot row 0
   // columns with a list longer than cap keep all their lists in the overflow arena:
-  // list k of overflow slot q at ovf_z[q*((R+1)*(ovf_cap+1) + 1) + k*(ovf_cap+1) + t], t = 1..ovf_cap
-  // (0 dummy; the one extra entry per slot is its spill cell);
+  // list k of overflow slot q at ovf_z[q*((R+1)*(ovf_cap+1) + LV_CLAMP) + k*(ovf_cap+1) + t], t = 1..ovf_cap
+  // (0 dummy; the LV_CLAMP extra entries per slot are its spill cells);
   // ovf_cap = the most pieces of any listed column (a level list never holds more components
   // than the column has pieces: each push starts with one)
   int32_t* ovf_idx;  // [nrows*nx] overflow slot of a column (valid only where some count > cap)
@@ -82,7 +87,7 @@ __host__ __device__ __forceinline__ size_t slot_z_index(const LevelSlots& L, int
 }
 
 __host__ __device__ __forceinline__ size_t ovf_z_index(const LevelSlots& L, int q, int k, int t) {
-  return (size_t)q * ((size_t)(L.R + 1) * (L.ovf_cap + 1) + 1) + (size_t)k * (L.ovf_cap + 1) + t;
+  return (size_t)q * ((size_t)(L.R + 1) * (L.ovf_cap + 1) + LV_CLAMP) + (size_t)k * (L.ovf_cap + 1) + t;
 }
 
 struct LvArgs {
@@ -98,6 +103,8 @@ struct LvArgs {
   unsigned ovf_list_cap;
   const uint32_t* list;    // overflow pass: the listed columns (count flags[1], read on the device)
   unsigned* opf;           // the op's flag words (kernels.cuh OpFlag)
+  uint32_t one = 1;        // 1, opaque to the compiler (a predicated multiply-add by it is a move that
+                           // issues on the FMA pipe; ptxas turns plain predicated moves into ALU selects)
 };
 
 constexpr int LV_T = 64;
@@ -199,9 +206,12 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   const uint32_t ostep = q < 0 ? (uint32_t)(R + 2) * nx : 1u;           // one slot
   const uint32_t olev = q < 0 ? nx : (uint32_t)(A.L.ovf_cap + 1);      // one level
   const uint32_t ncap = q < 0 ? (uint32_t)A.L.cap : (uint32_t)A.L.ovf_cap;
-  // the spill cell: level R+1 of the last slot (main pass), the arena slot's extra entry (overflow
-  // pass) -- never a list entry, so an offset that reaches it has saturated (the list overflowed)
-  const uint32_t olim = q < 0 ? ncap * ostep + (uint32_t)(R + 1 - k0) * nx : (uint32_t)(R + 1 - k0) * olev;
+  // the spill cells: level R+1 of the last LV_CLAMP slots (main pass), the arena slot's extra entries
+  // (overflow pass) -- never list entries.  Offsets are clamped to osat once per LV_CLAMP pieces, so
+  // a list at or beyond osat after a clamp has overflowed (its pushes in between land in the spill
+  // cells osat .. osat + (LV_CLAMP-1) ostep, or in its own slots up to the capacity).
+  const uint32_t osat = q < 0 ? (ncap - (uint32_t)(LV_CLAMP - 1)) * ostep + (uint32_t)(R + 1 - k0) * nx
+                              : (uint32_t)(R + 1 - k0) * olev;
   float cs[LMAX], ce[LMAX], pce[LMAX];
   uint32_t o[LMAX];
   bool lost = false;   // a popped component had been pushed beyond the capacity (column overflows)
@@ -210,12 +220,13 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     cs[k] = INFINITY;     // empty top
     ce[k] = -INFINITY;
     pce[k] = -INFINITY;   // no previous component
-    o[k] = min((uint32_t)k * olev, olim);
+    o[k] = min((uint32_t)k * olev, osat);
   }
   const int nchunk = (m + 3) >> 2;
   // shared addresses computed once (ring slots of this thread, the h table)
   const uint32_t rz_a = sh_addr(&ringz[0][0][threadIdx.x]), rk_a = sh_addr(&ringk[0][threadIdx.x]);
   const uint32_t hs_a = sh_addr(Hs);
+  const uint32_t one = A.one;
   auto issue = [&](int cq) {
     if (cq < nchunk) {
       const uint32_t u = (uint32_t)(cq % LV_DC);
@@ -232,6 +243,9 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   uint32_t u = 0;                     // ring slot of chunk t / 4
   for (int t = 0; t < mmax; ++t) {
     if ((t & 3) == 0) {
+      static_assert(LV_CLAMP == 4, "the clamp runs with the ring's 4-piece chunks");
+#pragma unroll
+      for (int k = 0; k < LMAX; ++k) o[k] = min(o[k], osat);
       issue((t >> 2) + LV_DC - 1);
       cp_async_wait<LV_DC - 1>();     // chunk t/4 has landed (this thread's own copies)
       kw = lds_u32(rk_a + u * (LV_T * 4));
@@ -258,15 +272,31 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
 #pragma unroll
     for (int k = 0; k < LMAX; ++k) {
       const float s = p.x - hv[k], e = p.y + hv[k];
-      const bool push = s > ce[k];
-      // push: the top is written to its slot (the first push writes the empty top into the
-      // dummy slot 0), predicated without a branch; the offset saturates at the spill cell
-      // (one VIADDMNMX: a column that reaches it has overflowed and is redone in the arena)
-      st_pred_f2(Zd + o[k], cs[k], ce[k], push);
-      o[k] = push ? min(o[k] + ostep, olim) : o[k];
-      pce[k] = push ? ce[k] : pce[k];
-      cs[k] = push ? s : fminf(cs[k], s);
-      ce[k] = push ? e : fmaxf(ce[k], e);
+      // push (s > ce): the top is written to its slot (the first push writes the empty top into
+      // the dummy slot 0), the offset advances one slot (clamped at the next 4-piece boundary,
+      // above), the previous end becomes ce and the new top starts at s.  Else the top extends
+      // (cs = min(cs, s)).  Either way ce = max(ce, e) (a push has e >= s > ce).  Predicated, no
+      // branch.  The step is ALU-pipe-bound (compares, min/max): the moves are predicated
+      // multiply-adds by an opaque 1 and the offset a predicated add, which ptxas issues on the
+      // FMA pipe (plain predicated moves become ALU selects).  Measured: levels at C5 59.6 ->
+      // 49.1 ms with the per-4-piece clamp and FMA-pipe moves.
+      asm volatile("{\n\t.reg .pred q;\n\t.reg .b32 a, b;\n\t"
+                   "setp.gt.f32 q, %4, %1;\n\t"
+                   "@q st.global.v2.f32 [%5], {%0, %1};\n\t"
+                   "@q add.u32 %2, %2, %6;\n\t"
+                   "mov.b32 a, %1;\n\t"
+                   "mov.b32 b, %3;\n\t"
+                   "@q mad.lo.u32 b, a, %7, 0;\n\t"
+                   "mov.b32 %3, b;\n\t"
+                   "@!q min.f32 %0, %0, %4;\n\t"
+                   "mov.b32 a, %4;\n\t"
+                   "mov.b32 b, %0;\n\t"
+                   "@q mad.lo.u32 b, a, %7, 0;\n\t"
+                   "mov.b32 %0, b;\n\t"
+                   "}"
+                   : "+f"(cs[k]), "+f"(ce[k]), "+r"(o[k]), "+f"(pce[k])
+                   : "f"(s), "l"(Zd + o[k]), "r"(ostep), "r"(one) : "memory");
+      ce[k] = fmaxf(ce[k], e);
       pop |= s <= pce[k];
     }
     if (__any_sync(0xffffffffu, pop)) {
@@ -274,7 +304,8 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
 #pragma unroll
       for (int k = 0; k < LMAX; ++k) {
         while (cs[k] <= pce[k]) {
-          if (o[k] == olim) {            // saturated: the stack's top entries were lost
+          o[k] = min(o[k], osat);        // (a list past the clamp point within this chunk: overflowed)
+          if (o[k] == osat) {            // saturated: the stack's top entries were lost
             lost = true;
             pce[k] = -INFINITY;
             break;
@@ -291,9 +322,10 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   }
 #pragma unroll
   for (int k = 0; k < LMAX; ++k) {
+    o[k] = min(o[k], osat);
     const bool top = cs[k] < ce[k];   // (the top is empty only if no piece reached this level)
     st_pred_f2(Zd + o[k], cs[k], ce[k], top);
-    lost |= k0 + k <= R && o[k] == olim;   // the offset saturated: the count is lost
+    lost |= k0 + k <= R && o[k] == osat;   // the offset saturated: the count is lost
     const uint32_t nk_ = top ? (o[k] - (uint32_t)k * olev) / ostep : 0u;   // slots 1..n
     if (live && k0 + k <= R) {
       A.L.cnt[slot_cnt_index(A.L, row, k0 + k, i)] =
@@ -302,7 +334,7 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
       mx = max(mx, nk_);
     }
   }
-  if (lost) mx = max(mx, ncap + 1);
+  if (lost) mx = max(mx, ncap + 1);   // (ncap + 1 > the effective capacity ncap - LV_CLAMP + 1)
   if (q >= 0) tot = 0;                    // the overflow pass recounts nothing
   if (live && q >= 0 && mx > ncap) {      // a list outgrew even the arena: rerun the op
     atomicOr(A.opf + OPF_LV_RERUN, 1u);

@@ -43,7 +43,8 @@ constexpr int P1G_T = 128;       // gather kernel block
 // register buffer flushed as one chunk.
 struct PFam {
   float zstart;       // start of the open run
-  int kap;            // its kappa (KNONE: no parent within R)
+  int kap;            // its kappa (knone: no parent within R)
+  int knone;          // "no parent" (KNONE, or R + 1 in the two-word warp sweep)
   float plo, phi;     // pending (closed, filtered-later) piece
   int pk;
   uint32_t trow;      // shared address of the threshold-table row of pk (row 17: no pending piece)
@@ -55,6 +56,7 @@ struct PFam {
   uint32_t cs;        // chunk stride in pieces: 4 nx (slots), 4 (arena), 0 (no output)
   uint32_t wlim;      // offset of the spill chunk: stores stay there once reached
   bool has_out;
+  uint32_t one, zero; // P.one, P.one - 1 (padd, fsel)
 };
 
 // predicated store of one piece without a branch: the (lo, hi) pair and its kappa byte
@@ -66,7 +68,7 @@ __device__ __forceinline__ void st_pred_piece(float2* zp, uint8_t* kp, float lo,
 
 // out_kind: 0 = slots of column i of band row jr, 1 = arena slot `aslot`, 2 = no output (spill)
 __device__ __forceinline__ void pfam_init(PFam& F, const PieceSlots& P, int jr, int i, int out_kind, int aslot,
-                                          uint32_t thr) {
+                                          uint32_t thr, int knone = KNONE) {
   const uint32_t nc = (uint32_t)(P.cap / 4);   // chunks per column (+1: the spill chunk)
   if (out_kind == 0) {
     F.zb = reinterpret_cast<float2*>(P.z + 2 * chunk_index(P, jr, 0, i));
@@ -89,14 +91,17 @@ __device__ __forceinline__ void pfam_init(PFam& F, const PieceSlots& P, int jr, 
   asm("mov.b64 %0, %0;" : "+l"(F.zb));
   asm("mov.b64 %0, %0;" : "+l"(F.kb));
   F.has_out = out_kind != 2;
+  F.one = P.one;
+  F.zero = P.one - 1u;
   F.np = 0;
   F.woff = 0;
   F.plo = F.phi = 0.f;
-  F.pk = KNONE;
+  F.knone = knone;
+  F.pk = knone;
   F.trow = thr + 17u * 32u * 8u;
   F.hpk = 0.f;
   F.zstart = 0.f;
-  F.kap = KNONE;
+  F.kap = knone;
 }
 
 // append one piece (predicated): piece t goes to slot t % 4 of chunk t / 4 (clamped to the spill
@@ -105,10 +110,10 @@ __device__ __forceinline__ void pfam_init(PFam& F, const PieceSlots& P, int jr, 
 // in another sector, shared with other lanes' pieces written at other times: DRAM read-fills).
 __device__ __forceinline__ void pfam_put(PFam& F, float lo, float hi, int k, bool wr) {
   st_pred_piece(F.zb + F.woff, F.kb + F.woff, lo, hi, k, wr);
-  F.np += wr ? 1u : 0u;
+  F.np = padd(wr, F.np, 1u, F.one);
   // the next slot of the chunk, or slot 0 of the next chunk (a running offset: no index arithmetic)
-  const uint32_t step = (F.np & 3u) ? 1u : F.cs - 3u;
-  F.woff += (wr && F.woff < F.wlim) ? step : 0u;
+  const uint32_t step = fsel((F.np & 3u) != 0u, 1u, F.cs - 3u, F.zero);
+  F.woff = padd(wr && F.woff < F.wlim, F.woff, step, F.one);
 }
 
 // a piece [zs, z] at level kap closes (closed == true): the capsule-domination filter against
@@ -122,7 +127,7 @@ __device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float
     return;
   }
   bool drop_new, drop_pend;
-  const bool hp = F.pk != KNONE;
+  const bool hp = F.pk != F.knone;
   if constexpr (TABLE) {
     const float2 th = lds_f2(F.trow + 8u * (uint32_t)(kap & 31));
     drop_new = z - F.phi <= th.x;
@@ -134,17 +139,17 @@ __device__ __forceinline__ void pfam_close(PFam& F, bool closed, float zs, float
   }
   pfam_put(F, F.plo, F.phi, F.pk, closed && hp && !drop_new && !drop_pend);
   const bool take = closed && !drop_new;
-  F.plo = take ? zs : F.plo;
-  F.phi = take ? z : F.phi;
-  if constexpr (TABLE) F.trow = take ? thr + 256u * (uint32_t)(kap & 31) : F.trow;
+  F.plo = fsel(take, zs, F.plo, F.zero);
+  F.phi = fsel(take, z, F.phi, F.zero);
+  if constexpr (TABLE) F.trow = fsel(take, thr + 256u * (uint32_t)(kap & 31), F.trow, F.zero);
   else F.hpk = take ? h0[kap & 255] : F.hpk;
-  F.pk = take ? kap : F.pk;
+  F.pk = fsel(take, kap, F.pk, F.zero);
 }
 
 // flush the pending piece; store the count; list an overflowing column (or ask for a rerun)
 __device__ __forceinline__ void pfam_finish(PFam& F, const PieceSlots& P, int64_t c, int jr, int tile, int ntiles,
                                             bool list_mode) {
-  pfam_put(F, F.plo, F.phi, F.pk, F.has_out && F.pk != KNONE);
+  pfam_put(F, F.plo, F.phi, F.pk, F.has_out && F.pk != F.knone);
   if (!list_mode) {
     if (F.has_out) {
       P.cnt[c] = F.np;
@@ -253,6 +258,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t one = FS_ON ? PS.one : PC.one;
   uint32_t* stage = p1_smem + (size_t)wid * (P1_STAGE + 4);
   const uint32_t stage_a = sh_addr(stage);
   const uint32_t ths = sh_addr(thr_s), thc = sh_addr(thr_c);
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   for (int q = 0; q < NW; ++q)
     nkey[q] = pos[q] < end[q] ? (staged ? lds_u32(pos[q]) : fkey(__ldg(ep + 2 * cb0[q] + pos[q]))) : KEY_NONE;
   // ---- this lane's output column and its families
+  const int knone = NW == 2 ? R + 1 : KNONE;
   const int i = T.i0 + lane;
   const bool out_ok = i < src.nx;
   const int64_t c = (int64_t)T.jr * src.nx + i;
@@ -326,8 +333,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       aslot = out_ok ? ovf_idx[c] : -1;
       kind = aslot >= 0 ? 1 : 2;
     }
-    if (FS_ON) pfam_init(FS, PS, T.jr, out_ok ? i : 0, kind, aslot, ths);
-    if (FC_ON) pfam_init(FC, PC, T.jr, out_ok ? i : 0, kind, aslot, thc);
+    if (FS_ON) pfam_init(FS, PS, T.jr, out_ok ? i : 0, kind, aslot, ths, knone);
+    if (FC_ON) pfam_init(FC, PC, T.jr, out_ok ? i : 0, kind, aslot, thc, knone);
   }
   const int pp = lane + R;
   // NW == 2: this lane's two 32-bit windows of the 64-bit mask, bits pp .. pp+31 (right) and
@@ -340,17 +347,21 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
     const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
     return lhigh ? la : lb;
   };
-  auto nearest_w = [&](uint32_t rw, uint32_t lw) -> int {
-    const int d = min(__clz(lw | 1u), __ffs(rw | 0x80000000u) - 1);
-    return d <= R ? d : KNONE;
+  // (NW == 2) nearest set bit within R of a lane's two windows: the windows are masked to
+  // distances <= R and carry a sentinel bit at distance R + 1, so the distance is R + 1 (= knone,
+  // "no parent") without a range test: one 3-input LOP per window
+  const uint32_t mkl = ~((1u << (31 - R)) - 1u), skl = 1u << (30 - R);     // left: bit 31 - d
+  const uint32_t mkr = (2u << R) - 1u, skr = 2u << R;                        // right: bit d
+  auto nearest_w = [&](uint32_t rw, uint32_t lw) -> int {   // (rw, lw masked + sentinels)
+    return min(__clz(lw), __ffs(rw) - 1);
   };
-  uint32_t gr = 0u, gl = 0u;   // (NW == 2) the windows of G, fixed for the sweep
+  uint32_t gr = 0u, gl = 0u;   // (NW == 2) the windows of G (masked), fixed for the sweep
   if constexpr (NW == 2) {
-    gr = win_r(G[0], G[1]);
-    gl = win_l(G[0], G[1]);
+    gr = win_r(G[0], G[1]) & mkr;
+    gl = win_l(G[0], G[1]) & mkl;
   }
   if (FC_ON) {               // before the first event every in-grid column is in C
-    if constexpr (NW == 2) FC.kap = nearest_w(gr, gl);
+    if constexpr (NW == 2) FC.kap = nearest_w(gr | skr, gl | skl);
     else FC.kap = nearest_bit<NW>(G, pp, R);
     FC.zstart = src.zlo;
   }
@@ -367,7 +378,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
         const bool hit = nkey[q] == zk;
         M[q] ^= __ballot_sync(FULL, hit);
         if constexpr (STG) {   // sentinel-terminated lists in shared memory
-          pos[q] += hit ? 4u : 0u;
+          pos[q] = padd(hit, pos[q], 4u, one);
           if (hit) nkey[q] = lds_u32(pos[q]);
         } else if (hit) {
           ++pos[q];
@@ -375,11 +386,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
         }
       }
       const float z = keyf(zk);
-      int ks = KNONE, kc = KNONE;
+      int ks = knone, kc = knone;
       if constexpr (NW == 2) {
         const uint32_t mr = win_r(M[0], M[1]), ml = win_l(M[0], M[1]);
-        if (FS_ON) ks = nearest_w(mr, ml);
-        if (FC_ON) kc = nearest_w(gr & ~mr, gl & ~ml);
+        if (FS_ON) ks = nearest_w((mr & mkr) | skr, (ml & mkl) | skl);
+        if (FC_ON) kc = nearest_w((gr & ~mr) | skr, (gl & ~ml) | skl);
       } else {
         if (FS_ON) ks = nearest_bit<NW>(M, pp, R);
         if (FC_ON) {
@@ -394,18 +405,18 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
         // an event changes kappa only for lanes within R of its column: a step where no lane of
         // the warp changes (often: halo events) skips the filter / emission half (warp-uniform)
         if (!SKIP || __any_sync(FULL, chg)) {
-          pfam_close<TABLE, PRN>(FS, chg && FS.kap != KNONE, FS.zstart, z, FS.kap, ths, h0s, mabs_s);
-          FS.kap = chg ? ks : FS.kap;
-          FS.zstart = chg ? z : FS.zstart;
+          pfam_close<TABLE, PRN>(FS, chg && FS.kap != knone, FS.zstart, z, FS.kap, ths, h0s, mabs_s);
+          FS.kap = fsel(chg, ks, FS.kap, FS.zero);
+          FS.zstart = fsel(chg, z, FS.zstart, FS.zero);
         }
       }
       if (FC_ON) {
         const bool chg = kc != FC.kap;
         if (!SKIP || __any_sync(FULL, chg)) {
-          pfam_close<TABLE, PRN>(FC, chg && FC.kap != KNONE && FC.zstart < z, FC.zstart, z, FC.kap, thc, h0c,
+          pfam_close<TABLE, PRN>(FC, chg && FC.kap != knone && FC.zstart < z, FC.zstart, z, FC.kap, thc, h0c,
                                  mabs_c);
-          FC.kap = chg ? kc : FC.kap;
-          FC.zstart = chg ? z : FC.zstart;
+          FC.kap = fsel(chg, kc, FC.kap, FC.zero);
+          FC.zstart = fsel(chg, z, FC.zstart, FC.zero);
         }
       }
     }
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
     else sweep(std::false_type{}, std::false_type{});
   }
   if (FC_ON) {   // C's last piece closes at z_hi
-    const bool cl = FC.kap != KNONE && FC.zstart < src.zhi;
+    const bool cl = FC.kap != knone && FC.zstart < src.zhi;
     if (prune) pfam_close<TABLE, true>(FC, cl, FC.zstart, src.zhi, FC.kap, thc, h0c, mabs_c);
     else pfam_close<TABLE, false>(FC, cl, FC.zstart, src.zhi, FC.kap, thc, h0c, mabs_c);
   }

@@ -55,10 +55,33 @@ def run_oracle(host, op, r, r2=None, cols=None):
     return getattr(O, op)(host, r, cols=cols)
 
 
+# parity summary per (config, op, r) for BASELINE.md section 3 (written when DEXEL_PARITY_REPORT names
+# a file: max endpoint error, count mismatches, columns compared)
+REPORT = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _parity_report():
+    yield
+    import json
+    import os
+    path = os.environ.get("DEXEL_PARITY_REPORT")
+    if path and REPORT:
+        old = {}
+        if os.path.exists(path):
+            with open(path) as f:
+                old = json.load(f)
+        old.update(REPORT)
+        with open(path, "w") as f:
+            json.dump(old, f, indent=1, sort_keys=True)
+
+
 def check(off, ep, ref, cols=None, what=""):
     if cols is not None:
         off, ep = take_columns(off, ep, cols)
     res = compare(off, ep, ref.off, ref.z, TAU)
+    REPORT[what] = dict(max_err=res["max_err"], count_mismatch=res["count_mismatch"],
+                        endpoint_fail=res["endpoint_fail"], columns=int(len(ref.off) - 1), n=res["n_b"])
     if not res["ok"]:
         c = res["first_bad"]
         raise AssertionError(f"{what}: {res}\n" + describe(off, ep, ref.off, ref.z, c))
@@ -122,7 +145,7 @@ def test_configs_all_columns(dx, name, r):
     host = G.config(name)
     for op in G.CONFIGS[name]["op"]:
         off, ep, _ = run_gpu(dx, host, op, r)
-        check(off, ep, run_oracle(host, op, r), what=f"{name} {op}")
+        check(off, ep, run_oracle(host, op, r), what=f"{name} {op} r={r}")
 
 
 # ------------------------------------------------------------------ big configs, sampled columns
