@@ -338,14 +338,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
   }
   const int pp = lane + R;
   // NW == 2: this lane's two 32-bit windows of the 64-bit mask, bits pp .. pp+31 (right) and
-  // pp-31 .. pp with bit pp on top (left); a sentinel bit at distance 31 > R keeps both non-zero
-  const int shr = pp < 32 ? pp : pp - 32;
-  const int shl = pp >= 31 ? pp - 31 : 31 - pp;
-  const bool rlow = pp < 32, lhigh = pp >= 31;
-  auto win_r = [&](uint32_t m0, uint32_t m1) { return __funnelshift_r(rlow ? m0 : m1, rlow ? m1 : 0u, shr); };
+  // pp-31 .. pp with bit pp on top (left), one 64-bit funnel shift each (SHF.R.U64 /
+  // SHF.L.U64.HI take shift amounts up to 63)
+  const uint32_t shl = (uint32_t)(63 - pp);
+  auto win_r = [&](uint32_t m0, uint32_t m1) {
+    return (uint32_t)((((unsigned long long)m1 << 32) | m0) >> pp);
+  };
   auto win_l = [&](uint32_t m0, uint32_t m1) {
-    const uint32_t la = __funnelshift_r(m0, m1, shl), lb = __funnelshift_l(0u, m0, shl);
-    return lhigh ? la : lb;
+    return (uint32_t)(((((unsigned long long)m1 << 32) | m0) << shl) >> 32);
   };
   // (NW == 2) nearest set bit within R of a lane's two windows: the windows are masked to
   // distances <= R and carry a sentinel bit at distance R + 1, so the distance is R + 1 (= knone,
