@@ -1095,7 +1095,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
     // unions longer than a shared-memory accumulator holds: a global one for the band's columns
     float2* gacc = nullptr;
     if (pass2_smem_bytes(op, acc, 32) > P2_SMEM_MAX &&
-        (s = T.get(sizeof(float2) * (size_t)acc * band * nx + 16, (void**)&gacc)))
+        (s = T.get(sizeof(float2) * (size_t)(acc + 2) * band * nx + 16, (void**)&gacc)))
       return s;
     CK(cudaMemsetAsync(opf, 0, sizeof(unsigned) * OPF_WORDS, st));
     uint32_t lev_cap_used = 0;
@@ -1202,7 +1202,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       acc = nacc;
       // (the handle keeps at most the largest shared-memory accumulator: one pathological op does
       // not send later ops to the global one)
-      src->p2_acc = std::min(acc, (int)(P2_SMEM_MAX / (32 * sizeof(float2))) - P2_R);
+      src->p2_acc = std::min(acc, (int)(P2_SMEM_MAX / (32 * sizeof(float2))) - 2 * P2_R - 2);
     }
     T.release(stage);
   }

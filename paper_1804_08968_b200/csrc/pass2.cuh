@@ -26,152 +26,160 @@ namespace dexel {
 
 enum { OP_DILATE = 0, OP_ERODE = 1, OP_SHELL = 2 };
 
-// In-place running union: acc[0..n) (shared memory, stride T) holds sorted disjoint closed
-// intervals.  Elements of one sorted list are inserted in order with a monotone cursor:
-// an element inside an accumulator interval costs a compare (the common case -- most of
-// the 4R+2 lists of a column fall inside what L_0 and the near rows already cover); an
-// element that reaches outside merges the overlapped run of intervals and shifts the tail.
-// Returns the new count (> cap: overflow, contents truncated).
+// In-place running union: acc[0..n) (shared memory, stride T; or global) holds sorted disjoint
+// closed intervals, followed by a sentinel acc[n] = (+inf, +inf), so cursor scans need no bound
+// test.  The elements of one sorted list are inserted in order with a monotone cursor p (the first
+// interval whose end reaches the element's start); w caches acc[p] and n1 the next interval's start,
+// so an element that is covered by w, or extends w without reaching the next interval -- the common
+// cases: most of the 4R+2 lists of a column fall inside or at the edges of what L_0 and the near rows
+// already cover -- costs two compares, a min / max and a store.  Anything else (a disjoint element:
+// insert and shift the tail; an element reaching the next interval: merge the run) takes the
+// general path.  A union longer than `cap` raises *need (the host reruns with a larger accumulator).
 struct Acc {
   float2* v;   // v[t * s]: shared memory (s = T, a compile-time constant) or global (the band's columns)
   int64_t s;
   int n;
 };
 
-template <int T>
-__device__ __forceinline__ void acc_insert(Acc& A, int& p, float2& w, float a, float b, int cap, unsigned* need) {
-  // p: first index with v[p].y >= a (monotone over one list, since the list's starts increase);
-  // w caches v[p] (valid while p < n), so an element covered at the cursor costs no load
-  while (p < A.n && w.y < a) {
-    ++p;
-    if (p < A.n) w = A.v[p * A.s];
-  }
-  if (p < A.n) {
-    if (w.x <= a && b <= w.y) return;                 // covered
-    if (w.x <= b) {                                   // overlaps [w.x, w.y]: merge the run p..q
-      int q = p;
-      float e = fmaxf(b, w.y);
-      while (q + 1 < A.n && A.v[(q + 1) * A.s].x <= e) { ++q; e = fmaxf(e, A.v[q * A.s].y); }
-      w = make_float2(fminf(a, w.x), e);
-      A.v[p * A.s] = w;
-      const int drop = q - p;
-      if (drop) {
-        for (int t = q + 1; t < A.n; ++t) A.v[(t - drop) * A.s] = A.v[t * A.s];
-        A.n -= drop;
-      }
-      return;
-    }
-  }
-  // disjoint from everything: insert before p (shift the tail right)
-  if (A.n >= cap) { *need = max(*need, (unsigned)(A.n + 1)); return; }
-  for (int t = A.n; t > p; --t) A.v[t * A.s] = A.v[(t - 1) * A.s];
-  w = make_float2(a, b);
-  A.v[p * A.s] = w;
-  ++A.n;
-}
-
-constexpr int P2_R = 8;   // list elements loaded per batch
-
-// insert a sorted list (element e at B[e * stride]) into the accumulator, P2_R elements at a
-// time: the batch's loads are independent and issue together (unrolled), the batch is parked in
-// a per-thread shared scratch and inserted by a rolled loop -- one inlined copy of acc_insert
-// keeps the kernel small enough for the instruction cache.  (Level sets are stored unclipped:
-// each element is clipped to [zlo, zhi] here; clipping commutes with the union.)
-// one batch (<= P2_R elements) of a sorted list: element e at B[e * stride]
-struct P2Batch {
-  float2 x[P2_R];
-  int n;
+struct Cursor {
+  int p;
+  float2 w;    // v[p]
+  float n1;    // v[p + 1].x (p < n; +inf at the sentinel)
 };
 
-template <int T>
-__device__ __forceinline__ void p2_load(P2Batch& X, const float2* __restrict__ B, int nb, int64_t stride) {
-  X.n = min(P2_R, nb);
-#pragma unroll
-  for (int u = 0; u < P2_R; ++u)
-    if (u < X.n) X.x[u] = B[(int64_t)u * stride];
+__device__ __forceinline__ void cur_load(const Acc& A, Cursor& C) {
+  C.w = A.v[C.p * A.s];
+  C.n1 = C.p < A.n ? A.v[(C.p + 1) * A.s].x : INFINITY;
 }
 
-// insert a loaded batch: parked in a per-thread shared scratch and inserted by a rolled loop --
-// one inlined copy of acc_insert keeps the kernel small enough for the instruction cache.
-// (Level sets are stored unclipped: each element is clipped to [zlo, zhi] here; clipping
-// commutes with the union.)
-template <int T>
-__device__ __forceinline__ void p2_insert(Acc& A, int& p, float2& w, const P2Batch& X, float2* scratch, float zlo,
-                                          float zhi, int cap, unsigned* need) {
-#pragma unroll
-  for (int u = 0; u < P2_R; ++u)
-    if (u < X.n) scratch[u * T] = X.x[u];
-#pragma unroll 1
-  for (int u = 0; u < X.n; ++u) {
-    const float2 v = scratch[u * T];
-    const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
-    if (lo < hi) acc_insert<T>(A, p, w, lo, hi, cap, need);
+// one element [a, b] (clipped, a < b) of a list, cursor C of this list
+__device__ __forceinline__ void acc_add(Acc& A, Cursor& C, float a, float b, int cap, unsigned* need) {
+  while (C.w.y < a) {   // (the sentinel stops it)
+    ++C.p;
+    cur_load(A, C);
   }
-}
-
-// insert a sorted list whose first batch X is already loaded (the rare rest batch by batch)
-template <int T>
-__device__ __forceinline__ void acc_insert_list(Acc& A, const P2Batch& X0, const float2* __restrict__ B, int nb,
-                                                int64_t stride, float2* scratch, float zlo, float zhi, int cap,
-                                                unsigned* need) {
-  int p = 0;
-  float2 w = A.n > 0 ? A.v[0] : make_float2(0.f, 0.f);
-  p2_insert<T>(A, p, w, X0, scratch, zlo, zhi, cap, need);
-  for (int e0 = P2_R; e0 < nb; e0 += P2_R) {
-    P2Batch X;
-    p2_load<T>(X, B + (int64_t)e0 * stride, nb - e0, stride);
-    p2_insert<T>(A, p, w, X, scratch, zlo, zhi, cap, need);
+  if (b >= C.w.x && b < C.n1) {   // covered by w, or extends w within the gap before the next one
+    C.w = make_float2(fminf(a, C.w.x), fmaxf(b, C.w.y));
+    A.v[C.p * A.s] = C.w;
+    return;
   }
+  if (b < C.w.x) {   // disjoint: insert before p (at p == n: append), shifting the tail and the sentinel
+    if (A.n >= cap) {
+      *need = max(*need, (unsigned)(A.n + 1));
+      return;
+    }
+    for (int t = A.n; t >= C.p; --t) A.v[(t + 1) * A.s] = A.v[t * A.s];
+    ++A.n;
+    C.n1 = C.w.x;
+    C.w = make_float2(a, b);
+    A.v[C.p * A.s] = C.w;
+    return;
+  }
+  // overlaps w and reaches the next interval: merge the run
+  int q = C.p;
+  float e = fmaxf(b, C.w.y);
+  while (A.v[(q + 1) * A.s].x <= e) {   // (q + 1 <= n: the sentinel's +inf stops it)
+    ++q;
+    e = fmaxf(e, A.v[q * A.s].y);
+  }
+  C.w = make_float2(fminf(a, C.w.x), e);
+  A.v[C.p * A.s] = C.w;
+  const int drop = q - C.p;
+  for (int t = q + 1; t <= A.n; ++t) A.v[(t - drop) * A.s] = A.v[t * A.s];   // (incl. the sentinel)
+  A.n -= drop;
+  C.n1 = A.v[(C.p + 1) * A.s].x;
 }
 
-// union over dy of one family's level lists for output column (i, jg): for each row
-// offset dy = 0, 1, -1, 2, -2, ... the list L_|dy| of column (i, jg+dy).  The next row's
-// first batch is loaded before the current row is inserted (two rows' loads in flight), and
-// counts are read one row further ahead.
+constexpr int P2_R = 8;   // list elements fetched per batch
+
+// union over dy of one family's level lists for output column (i, jg): for each row offset
+// dy = 0, 1, -1, 2, -2, ... the list L_|dy| of column (i, jg+dy), in lockstep across the warp (every
+// list read is coalesced).  The first P2_R elements of the next list are copied into this thread's
+// half of a double-buffered shared scratch with cp.async while the current list is inserted (counts
+// are read one list further ahead); longer lists fetch the rest batch by batch.  Level sets are
+// stored unclipped: each element is clipped to [zlo, zhi] here (clipping commutes with the union).
 template <int T>
 __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, float zlo, float zhi, Acc& A,
-                                          float2* scratch, int cap, unsigned* need) {
+                                          uint32_t scr, int cap, unsigned* need) {
   A.n = 0;
+  A.v[0] = make_float2(INFINITY, INFINITY);
   const int dlo = max(-L.ry, L.row0 - jg), dhi = min(L.ry, L.row0 + L.nrows - 1 - jg);
   const int nt = 2 * L.ry + 1;
   auto dy_of = [](int t) { return (t & 1) ? ((t + 1) >> 1) : -(t >> 1); };
+  // row jg's counts and level slots; row jg + dy, level k at  + dy * (one row) + k * nx
+  const uint16_t* cnt0 = L.cnt + slot_cnt_index(L, jg - L.row0, 0, i);
+  const int64_t crow = (int64_t)(L.R + 1) * L.nx;
+  const float2* z0 = L.z + slot_z_index(L, jg - L.row0, 0, 1, i);
+  const int64_t zrow = (int64_t)(L.cap + 1) * (L.R + 2) * L.nx, zslot = (int64_t)(L.R + 2) * L.nx;
   auto count = [&](int t) -> int {
     if (t >= nt) return 0;
     const int dy = dy_of(t), k = dy < 0 ? -dy : dy;
-    return (dy < dlo || dy > dhi) ? 0 : (int)L.cnt[slot_cnt_index(L, jg + dy - L.row0, k, i)];
+    return (dy < dlo || dy > dhi) ? 0 : (int)cnt0[(int64_t)dy * crow + k * L.nx];
   };
-  // list of row offset t (count word cw != 0): first element's address and stride, first batch
-  // loaded; returns the list length
-  auto open = [&](int t, int cw, const float2*& lb, int64_t& st, P2Batch& X) -> int {
-    const int dy = dy_of(t), k = dy < 0 ? -dy : dy, jl = jg + dy - L.row0;
-    // (a slot list longer than cap that found no arena slot: the op reruns, read what exists)
-    const int nb = (cw & LV_IN_ARENA) ? (cw & LV_CNT_MAX) : min(cw & LV_CNT_MAX, L.cap);
+  // list t (count word cw != 0): its first element's address and stride, its length; the first
+  // batch is copied into scratch half h
+  auto open = [&](int t, int cw, const float2*& lb, int64_t& st, uint32_t h) -> int {
+    const int dy = dy_of(t), k = dy < 0 ? -dy : dy;
+    int nb;
     if (!(cw & LV_IN_ARENA)) {
-      lb = L.z + slot_z_index(L, jl, k, 1, i);
-      st = (int64_t)(L.R + 2) * L.nx;   // one slot
-    } else {   // the column's lists live in the overflow arena
-      lb = L.ovf_z + ovf_z_index(L, L.ovf_idx[(size_t)jl * L.nx + i], k, 1);
+      // (a slot list longer than cap that found no arena slot: the op reruns, read what exists)
+      nb = min(cw & LV_CNT_MAX, L.cap);
+      lb = z0 + (int64_t)dy * zrow + k * L.nx;
+      st = zslot;
+    } else {   // (rare) the column's lists live in the overflow arena
+      nb = cw & LV_CNT_MAX;
+      lb = L.ovf_z + ovf_z_index(L, L.ovf_idx[(size_t)(jg + dy - L.row0) * L.nx + i], k, 1);
       st = 1;
     }
-    p2_load<T>(X, lb, nb, st);
+    const uint32_t sb = scr + h * (uint32_t)(P2_R * T * 8);
+#pragma unroll
+    for (int u = 0; u < P2_R; ++u)
+      if (u < nb) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + (uint32_t)(u * T * 8)),
+                               "l"(lb + u * st));
     return nb;
   };
   int cw = count(0), cwn = count(1), n = 0;
   const float2* lb = nullptr;
   int64_t st = 0;
-  P2Batch X;
-  X.n = 0;
-  if (cw & LV_CNT_MAX) n = open(0, cw, lb, st, X);
+  uint32_t h = 0;
+  if (cw & LV_CNT_MAX) n = open(0, cw, lb, st, 0);
+  asm volatile("cp.async.commit_group;\n" ::);
   for (int t = 0; t < nt; ++t) {
     const int nc = n;
     const float2* lbc = lb;
     const int64_t stc = st;
-    const P2Batch Xc = X;
+    const uint32_t hc = h;
     cw = cwn;
     cwn = count(t + 2);
-    n = (cw & LV_CNT_MAX) ? open(t + 1, cw, lb, st, X) : 0;
-    if (nc) acc_insert_list<T>(A, Xc, lbc, nc, stc, scratch, zlo, zhi, cap, need);
+    h ^= 1u;
+    n = (cw & LV_CNT_MAX) ? open(t + 1, cw, lb, st, h) : 0;
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);   // list t's batch has landed
+    if (nc) {
+      Cursor C{0, A.v[0], A.n > 0 ? A.v[A.s].x : INFINITY};
+      const uint32_t sb = scr + hc * (uint32_t)(P2_R * T * 8);
+      for (int e0 = 0; e0 < nc; e0 += P2_R) {
+        if (e0 > 0) {   // (a list longer than P2_R) its next batch into the same half, then wait for it
+#pragma unroll
+          for (int u = 0; u < P2_R; ++u)
+            if (e0 + u < nc)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + (uint32_t)(u * T * 8)),
+                           "l"(lbc + (e0 + u) * stc));
+          asm volatile("cp.async.commit_group;\n" ::);
+          asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        const int nu = min(nc - e0, P2_R);
+#pragma unroll 1
+        for (int u = 0; u < nu; ++u) {
+          float2 v;
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sb + (uint32_t)(u * T * 8)));
+          const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
+          if (lo < hi) acc_add(A, C, lo, hi, cap, need);
+        }
+      }
+    }
   }
+  asm volatile("cp.async.wait_all;\n" ::);
 }
 
 // output rows [row0, row0 + nrows_out) (extended-row numbering of the level slots) of a band;
@@ -196,9 +204,11 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
   const int64_t c = cbase + cl;
   const int jg = row0 + jr;
   unsigned need = 0;
+  // shared memory: the accumulators [acc + 2][T] (+ the sentinel; unless global), the list scratch
+  // [2][P2_R][T]
   Acc U = GACC ? Acc{gacc + cl, (int64_t)nrows_out * nx, 0} : Acc{p2_smem + tid, T, 0};
-  float2* scratch = p2_smem + (GACC ? 0 : (size_t)acc * T) + tid;     // [P2_R][T]
-  p2_family<T>(A, i, jg, zlo, zhi, U, scratch, acc, &need);
+  const uint32_t scr = (uint32_t)__cvta_generic_to_shared(p2_smem + (GACC ? 0 : (size_t)(acc + 2) * T) + tid);
+  p2_family<T>(A, i, jg, zlo, zhi, U, scr, acc, &need);
   uint32_t n = 0;
   if (OP == OP_DILATE) {
     for (int t = 0; t < U.n; ++t) ostage[(size_t)t * ncol + c] = U.v[t * U.s];
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
     for (int t = 0; t < nu; ++t) ostage[(size_t)(acc + t) * ncol + c] = U.v[t * U.s];
     // D_rin(C) only matters inside D_rout(S): an empty D(S) skips it, and its list elements are
     // clipped to D(S)'s hull instead of [z_lo, z_hi] (fewer insertions, a shorter accumulator)
-    if (nu > 0) p2_family<T>(B, i, jg, U.v[0].x, U.v[(nu - 1) * U.s].y, U, scratch, acc, &need);
+    if (nu > 0) p2_family<T>(B, i, jg, U.v[0].x, U.v[(nu - 1) * U.s].y, U, scr, acc, &need);
     else U.n = 0;
     int p = 0, q = 0;
     float2 u = nu > 0 ? ostage[(size_t)acc * ncol + c] : make_float2(0.f, 0.f);
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
 
 inline size_t pass2_smem_bytes(int op, int acc, int T, bool gacc = false) {
   (void)op;
-  return (size_t)((gacc ? 0 : acc) + P2_R) * T * sizeof(float2);
+  return (size_t)((gacc ? 0 : acc + 2) + 2 * P2_R) * T * sizeof(float2);
 }
 constexpr size_t P2_SMEM_MAX = 220 * 1024;   // shared memory an accumulator block may take
 inline int pass2_stage_cap(int op, int acc) { return op == OP_SHELL ? 2 * acc : acc + 1; }
