@@ -4,7 +4,7 @@
 # the ncu launch list of the default bench command, and --gpus 2 on a 1-GPU box (must fail loudly).
 # usage: bash tools/gpu_final.sh TAG [matrix steps]
 tag=${1:-final}; steps=${2:-10}
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest.log 2>&1
+DEXEL_PARITY_REPORT=gpurun_out/${tag}_parity.json timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
 timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/${tag}_smoke.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/${tag}_smoke.log
