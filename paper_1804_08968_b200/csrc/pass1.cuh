@@ -33,7 +33,10 @@
 
 namespace dexel {
 
-constexpr int P1_WARPS = 4;
+#ifndef P1_WARPS_N
+#define P1_WARPS_N 4
+#endif
+constexpr int P1_WARPS = P1_WARPS_N;
 constexpr int P1_STAGE = 2048;   // staged window keys per warp (larger windows read through L1)
 constexpr int P1G_RMAX = 4;      // gather kernel up to this R (measured)
 constexpr int P1G_T = 128;       // gather kernel block

@@ -90,7 +90,10 @@ __device__ __forceinline__ void acc_add(Acc& A, Cursor& C, float a, float b, int
   C.n1 = A.v[(C.p + 1) * A.s].x;
 }
 
-constexpr int P2_R = 8;   // list elements fetched per batch
+#ifndef P2_R_N
+#define P2_R_N 6
+#endif
+constexpr int P2_R = P2_R_N;   // list elements fetched per batch
 
 // union over dy of one family's level lists for output column (i, jg): for each row offset
 // dy = 0, 1, -1, 2, -2, ... the list L_|dy| of column (i, jg+dy), in lockstep across the warp (every
