@@ -269,9 +269,24 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     // the first chunk never skips -- the test, which waits on the table load, runs from k0 > 0.)
     if (k0 > 0 && __all_sync(0xffffffffu, isnan(hv[0]))) continue;
     bool pop = false;
+    // the grown ends of all levels first, two levels per packed fp32 instruction (FADD2, sm_100a:
+    // one issue slot for two exact fp32 additions, the same rounding as two FADDs)
+    float sv[LMAX], ev[LMAX];
+#pragma unroll
+    for (int k = 0; k + 1 < LMAX; k += 2) {
+      asm("{\n\t.reg .b64 x, y, h, r;\n\tmov.b64 x, {%4, %4};\n\tmov.b64 y, {%5, %5};\n\t"
+          "mov.b64 h, {%6, %7};\n\tsub.rn.f32x2 r, x, h;\n\tmov.b64 {%0, %1}, r;\n\t"
+          "add.rn.f32x2 r, y, h;\n\tmov.b64 {%2, %3}, r;\n\t}"
+          : "=f"(sv[k]), "=f"(sv[k + 1]), "=f"(ev[k]), "=f"(ev[k + 1])
+          : "f"(p.x), "f"(p.y), "f"(hv[k]), "f"(hv[k + 1]));
+    }
+    if constexpr (LMAX & 1) {
+      sv[LMAX - 1] = p.x - hv[LMAX - 1];
+      ev[LMAX - 1] = p.y + hv[LMAX - 1];
+    }
 #pragma unroll
     for (int k = 0; k < LMAX; ++k) {
-      const float s = p.x - hv[k], e = p.y + hv[k];
+      const float s = sv[k], e = ev[k];
       // push (s > ce): the top is written to its slot (the first push writes the empty top into
       // the dummy slot 0), the offset advances one slot (clamped at the next 4-piece boundary,
       // above), the previous end becomes ce and the new top starts at s.  Else the top extends
