@@ -16,20 +16,20 @@
 //     L_k = U_p [lo_p - h, hi_p + h]    (= U_f(k) u U_r(k) with U_f = U_p [lo_p, hi_p + h] and
 //                                         U_r = U_p [lo_p - h, hi_p], the two half-space parts)
 // The pieces are sorted and disjoint, so their grown intervals come in ascending lo_p but
-// not ascending lo_p - h.  One forward sweep builds L_k with a stack of components (the
-// half-space envelope's stack, restated for level sets): the top
+// not ascending lo_p - h.  One forward sweep builds L_k as a list of components (the
+// half-space envelope's sweep, restated for level sets): the top
 // component [cs, ce] lives in registers; a grown interval starting above ce closes it
-// (push: written to the level's slots), otherwise it extends it -- and when its start
-// reaches below the previous component's end pce (a small-kappa piece swallowing a gap
-// left by out-of-reach pieces) that component is popped back from the slots.  Pops are
-// rare (measured on C5: ~1-3 per column per ~3000 (piece, level) steps, never deeper than
-// one), so they run in a warp-uniform side branch; the main step is two fp32 adds, a few
-// compares/selects and a predicated store -- no branches, no square roots (the h table is
-// fp64 on the host, rounded once to fp32, reading R20).  A thread owns one
-// column and a chunk of LMAX levels held in registers (blockIdx.y = chunk), so the kernel
-// is SIMT-uniform.  (An explicit upper-envelope variant ran 4-6x slower -- 4 of 32 lanes
-// active; two half-space sweeps U_f / U_r in separate threads plus a merge ran ~1.5x
-// slower: DESIGN.md "What was tried".)
+// (push: written to the level's slots), otherwise it extends it.  A grown interval that
+// reaches below the end of components pushed earlier (a small-kappa piece swallowing a gap
+// left by out-of-reach pieces; ~1-3 times per column per ~3000 (piece, level) steps on C5)
+// is not merged with them: the list stays sorted by component end and pass 2, a union,
+// takes it as it is (its cursor restarts where a list's starts decrease).  So the main step
+// is two fp32 adds (one packed FADD2 per two levels), two compares / min-max and a
+// predicated store -- no branches, no square roots (the h table is fp64 on the host,
+// rounded once to fp32, reading R20).  A thread owns one column and a chunk of
+// LMAX levels held in registers (blockIdx.y = chunk), so the kernel is SIMT-uniform.  (An
+// explicit upper-envelope variant ran 4-10x slower; two half-space sweeps U_f / U_r in
+// separate threads plus a merge ran ~1.5x slower: DESIGN.md "What was tried".)
 //
 // Input: pass-1 piece chunks (kernels.cuh PieceSlots) through a cp.async ring.
 // Layout (HBM): level slots  z[((row*(cap+1) + t)*(R+2) + k)*nx + i]  (float2), t = 1..cap
@@ -37,10 +37,8 @@
 // counts cnt[(row*(R+1) + k)*nx + i] (u16).  For a fixed (row, k, t) the nx columns of a
 // row are contiguous, so a warp of 32 consecutive columns writes and (in pass 2) reads
 // 256 contiguous bytes.  A list longer than cap raises a flag: the column is listed and
-// an overflow pass rewrites all its lists into an arena of m-entry lists (m = the most pieces of
-// any listed column) and flags their
-// counts (LV_IN_ARENA: a column can overflow mid-sweep and end with every count <= cap
-// after pops, so the flag, not the count, tells pass 2 where a list is); if too many
+// an overflow pass rewrites all its lists into an arena of lists and flags their counts
+// (LV_IN_ARENA: the flag, not the count, tells pass 2 where a list is); if too many
 // columns overflow the host reruns the band with a larger cap.
 #pragma once
 #include <cstdint>
@@ -140,7 +138,7 @@ struct LvTab {
 };
 
 template <int LMAX>
-__global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs A) {
+__global__ void __launch_bounds__(LV_T, 8) levels_kernel(LvArgs A) {
   constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
   __shared__ __align__(16) float Hs[257 * HS];   // h(kappa, k0 + k), NaN beyond R or out of reach;
                                                   // row R+1: all NaN (the "null piece")
@@ -212,14 +210,13 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
   // cells osat .. osat + (LV_CLAMP-1) ostep, or in its own slots up to the capacity).
   const uint32_t osat = q < 0 ? (ncap - (uint32_t)(LV_CLAMP - 1)) * ostep + (uint32_t)(R + 1 - k0) * nx
                               : (uint32_t)(R + 1 - k0) * olev;
-  float cs[LMAX], ce[LMAX], pce[LMAX];
+  float cs[LMAX], ce[LMAX];
   uint32_t o[LMAX];
-  bool lost = false;   // a popped component had been pushed beyond the capacity (column overflows)
+  bool lost = false;
 #pragma unroll
   for (int k = 0; k < LMAX; ++k) {
     cs[k] = INFINITY;     // empty top
     ce[k] = -INFINITY;
-    pce[k] = -INFINITY;   // no previous component
     o[k] = min((uint32_t)k * olev, osat);
   }
   const int nchunk = (m + 3) >> 2;
@@ -268,7 +265,6 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
     // (Level 0 is in reach of every real piece and t < mmax leaves some lane a real piece, so
     // the first chunk never skips -- the test, which waits on the table load, runs from k0 > 0.)
     if (k0 > 0 && __all_sync(0xffffffffu, isnan(hv[0]))) continue;
-    bool pop = false;
     // the grown ends of all levels first, two levels per packed fp32 instruction (FADD2, sm_100a:
     // one issue slot for two exact fp32 additions, the same rounding as two FADDs)
     float sv[LMAX], ev[LMAX];
@@ -289,50 +285,28 @@ __global__ void __launch_bounds__(LV_T, LMAX >= 12 ? 7 : 8) levels_kernel(LvArgs
       const float s = sv[k], e = ev[k];
       // push (s > ce): the top is written to its slot (the first push writes the empty top into
       // the dummy slot 0), the offset advances one slot (clamped at the next 4-piece boundary,
-      // above), the previous end becomes ce and the new top starts at s.  Else the top extends
-      // (cs = min(cs, s)).  Either way ce = max(ce, e) (a push has e >= s > ce).  Predicated, no
-      // branch.  The step is ALU-pipe-bound (compares, min/max): the moves are predicated
-      // multiply-adds by an opaque 1 and the offset a predicated add, which ptxas issues on the
-      // FMA pipe (plain predicated moves become ALU selects).  Measured: levels at C5 59.6 ->
-      // 49.1 ms with the per-4-piece clamp and FMA-pipe moves.
+      // above) and the new top starts at s.  Else the top extends (cs = min(cs, s)).  Either way
+      // ce = max(ce, e) (a push has e >= s > ce).  Predicated, no branch.  The step is issue-bound:
+      // the moves are predicated multiply-adds by an opaque 1 and the offset a predicated add, which
+      // ptxas issues on the FMA pipe (plain predicated moves become ALU selects).
+      // A top extended below the end of components pushed before it (a small-kappa piece swallowing
+      // a gap left by out-of-reach pieces: ~1-3 times per column per ~3000 steps on C5) is NOT merged
+      // with them here: the list stays sorted by component end, every component is a union of grown
+      // pieces, and pass 2 (a union) takes the components in any order -- so the sweep keeps no
+      // previous-end register and no merge test (2 of ~11 instructions per (piece, level)).
       asm volatile("{\n\t.reg .pred q;\n\t.reg .b32 a, b;\n\t"
-                   "setp.gt.f32 q, %4, %1;\n\t"
-                   "@q st.global.v2.f32 [%5], {%0, %1};\n\t"
-                   "@q add.u32 %2, %2, %6;\n\t"
-                   "mov.b32 a, %1;\n\t"
-                   "mov.b32 b, %3;\n\t"
-                   "@q mad.lo.u32 b, a, %7, 0;\n\t"
-                   "mov.b32 %3, b;\n\t"
-                   "@!q min.f32 %0, %0, %4;\n\t"
-                   "mov.b32 a, %4;\n\t"
+                   "setp.gt.f32 q, %3, %1;\n\t"
+                   "@q st.global.v2.f32 [%4], {%0, %1};\n\t"
+                   "@q add.u32 %2, %2, %5;\n\t"
+                   "@!q min.f32 %0, %0, %3;\n\t"
+                   "mov.b32 a, %3;\n\t"
                    "mov.b32 b, %0;\n\t"
-                   "@q mad.lo.u32 b, a, %7, 0;\n\t"
+                   "@q mad.lo.u32 b, a, %6, 0;\n\t"
                    "mov.b32 %0, b;\n\t"
                    "}"
-                   : "+f"(cs[k]), "+f"(ce[k]), "+r"(o[k]), "+f"(pce[k])
+                   : "+f"(cs[k]), "+f"(ce[k]), "+r"(o[k])
                    : "f"(s), "l"(Zd + o[k]), "r"(ostep), "r"(one) : "memory");
       ce[k] = fmaxf(ce[k], e);
-      pop |= s <= pce[k];
-    }
-    if (__any_sync(0xffffffffu, pop)) {
-      // rare: the extended top reaches the previous component -> pop it (and maybe more)
-#pragma unroll
-      for (int k = 0; k < LMAX; ++k) {
-        while (cs[k] <= pce[k]) {
-          o[k] = min(o[k], osat);        // (a list past the clamp point within this chunk: overflowed)
-          if (o[k] == osat) {            // saturated: the stack's top entries were lost
-            lost = true;
-            pce[k] = -INFINITY;
-            break;
-          }
-          const uint32_t j = o[k] - ostep;                      // the previous component's slot
-          const float2 pv = Zd[j];
-          cs[k] = fminf(cs[k], pv.x);
-          o[k] = j;
-          // the new previous component (the dummy slot 0 ends the stack: pce = -inf)
-          pce[k] = j - (uint32_t)k * olev > ostep ? Zd[j - ostep].y : -INFINITY;
-        }
-      }
     }
   }
 #pragma unroll

@@ -28,7 +28,7 @@ enum { OP_DILATE = 0, OP_ERODE = 1, OP_SHELL = 2 };
 
 // In-place running union: acc[0..n) (shared memory, stride T; or global) holds sorted disjoint
 // closed intervals, followed by a sentinel acc[n] = (+inf, +inf), so cursor scans need no bound
-// test.  The elements of one sorted list are inserted in order with a monotone cursor p (the first
+// test.  The elements of one list are inserted in order with a forward cursor p (the first
 // interval whose end reaches the element's start); w caches acc[p] and n1 the next interval's start,
 // so an element that is covered by w, or extends w without reaching the next interval -- the common
 // cases: most of the 4R+2 lists of a column fall inside or at the edges of what L_0 and the near rows
@@ -160,6 +160,7 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
     asm volatile("cp.async.wait_group 1;\n" ::);   // list t's batch has landed
     if (nc) {
       Cursor C{0, A.v[0], A.n > 0 ? A.v[A.s].x : INFINITY};
+      float alast = -INFINITY;
       const uint32_t sb = scr + hc * (uint32_t)(P2_R * T * 8);
       for (int e0 = 0; e0 < nc; e0 += P2_R) {
         if (e0 > 0) {   // (a list longer than P2_R) its next batch into the same half, then wait for it
@@ -177,7 +178,16 @@ __device__ __forceinline__ void p2_family(const LevelSlots& L, int i, int jg, fl
           float2 v;
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sb + (uint32_t)(u * T * 8)));
           const float lo = fmaxf(v.x, zlo), hi = fminf(v.y, zhi);
-          if (lo < hi) acc_add(A, C, lo, hi, cap, need);
+          if (lo < hi) {
+            // a level list is sorted by component end; a component may start below earlier ones
+            // (levels.cuh: not merged there) -- the cursor then restarts (rare)
+            if (lo < alast) {
+              C.p = 0;
+              cur_load(A, C);
+            }
+            alast = lo;
+            acc_add(A, C, lo, hi, cap, need);
+          }
         }
       }
     }
