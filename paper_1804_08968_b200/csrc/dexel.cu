@@ -403,7 +403,7 @@ dexel_status check_radius(float r, double s, int* R) {
 // one pass-1 launch of families `fams` (1 = S, 2 = C = U \ S, 3 = both, pass1.cuh): main mode
 // over slot rows [jr0, jr0 + nrows_out) of a band whose slot row 0 is extended row row0; list mode
 // (nlist >= 0, one family) over the listed tiles
-template <int NW, int F, bool TABLE, bool SKIP>
+template <int NW, int F, bool TABLE, int SKIP>
 void launch_p1s_t(unsigned blocks, cudaStream_t st, const SrcRows& src, int R, int row0, int jr0, int nrows_out,
                   const PieceSlots& PS, const PieceSlots& PC, int64_t nlist, const float* ps, const float* pc) {
   const size_t smem = p1s_smem();
@@ -439,12 +439,16 @@ void launch_p1_f(const SrcRows& src, int R, int row0, int jr0, int nrows_out, co
   if (blocks == 0) return;
   const int NW = (32 + 2 * R + 31) / 32;   // window words
 #define P1S(NWV, TB, SK) launch_p1s_t<NWV, F, TB, SK>(blocks, st, src, R, row0, jr0, nrows_out, PS, PC, nlist, ps, pc)
-  if (NW <= 2 && R < 8) P1S(2, true, false);   // (the step-skip vote pays from R = 8, measured)
-  else if (NW <= 2) P1S(2, true, true);
-  else if (NW <= 3) P1S(3, false, true);
-  else if (NW <= 5) P1S(5, false, true);
-  else if (NW <= 9) P1S(9, false, true);
-  else P1S(17, false, true);
+  // the step-skip vote (a warp vote per family and step) no longer pays for R <= 16 since the emission
+  // half moved to the FMA pipe (measured: C4 r = 8 pass 1 4.11 -> 3.83 ms without it, C5 equal); it
+  // stays for the larger windows.  DEXEL_P1_SKIP=1 forces it on (A/B).
+  static const int skip_mode = [] { const char* e = std::getenv("DEXEL_P1_SKIP"); return e ? std::atoi(e) : -1; }();
+  if (NW <= 2 && skip_mode != 1) P1S(2, true, 0);
+  else if (NW <= 2) P1S(2, true, 1);
+  else if (NW <= 3) P1S(3, false, 1);
+  else if (NW <= 5) P1S(5, false, 1);
+  else if (NW <= 9) P1S(9, false, 1);
+  else P1S(17, false, 1);
 #undef P1S
 }
 
@@ -1254,12 +1258,12 @@ void preload_p1() {
   preload_one(p1g_kernel<2, F>);
   preload_one(p1g_kernel<3, F>);
   preload_one(p1g_kernel<4, F>);
-  preload_one(p1s_kernel<2, F, true, false>);
-  preload_one(p1s_kernel<2, F, true, true>);
-  preload_one(p1s_kernel<3, F, false, true>);
-  preload_one(p1s_kernel<5, F, false, true>);
-  preload_one(p1s_kernel<9, F, false, true>);
-  preload_one(p1s_kernel<17, F, false, true>);
+  preload_one(p1s_kernel<2, F, true, 0>);
+  preload_one(p1s_kernel<2, F, true, 1>);
+  preload_one(p1s_kernel<3, F, false, 1>);
+  preload_one(p1s_kernel<5, F, false, 1>);
+  preload_one(p1s_kernel<9, F, false, 1>);
+  preload_one(p1s_kernel<17, F, false, 1>);
 }
 template <int OP>
 void preload_p2() {

@@ -238,7 +238,8 @@ __device__ __forceinline__ P1Tile p1_tile(const SrcRows& src, int row0, int64_t 
 // (SKIP, a warp vote: pays from R = 8).  (A batched variant -- window events recorded in shared
 // memory, per-lane emission only at the events that can change the lane's column -- walked fewer
 // emission steps but measured 1.2-1.5x slower at R >= 8: DESIGN.md "What was tried".)
-template <int NW, int FAMS, bool TABLE, bool SKIP>
+// SKIP: 0 = none, 1 = a warp vote per family and step (one vote for both families measured slower)
+template <int NW, int FAMS, bool TABLE, int SKIP>
 __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, int row0, int jr0, int nrows_out,
                                                              PieceSlots PS, PieceSlots PC, int64_t nlist,
                                                              const float* __restrict__ prune_s,
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
         const bool chg = ks != FS.kap;
         // an event changes kappa only for lanes within R of its column: a step where no lane of
         // the warp changes (often: halo events) skips the filter / emission half (warp-uniform)
-        if (!SKIP || __any_sync(FULL, chg)) {
+        if (SKIP != 1 || __any_sync(FULL, chg)) {
           pfam_close<TABLE, PRN>(FS, chg && FS.kap != knone, FS.zstart, z, FS.kap, ths, h0s, mabs_s);
           FS.kap = fsel(chg, ks, FS.kap, FS.zero);
           FS.zstart = fsel(chg, z, FS.zstart, FS.zero);
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32) p1s_kernel(SrcRows src, int R, 
       }
       if (FC_ON) {
         const bool chg = kc != FC.kap;
-        if (!SKIP || __any_sync(FULL, chg)) {
+        if (SKIP != 1 || __any_sync(FULL, chg)) {
           pfam_close<TABLE, PRN>(FC, chg && FC.kap != knone && FC.zstart < z, FC.zstart, z, FC.kap, thc, h0c,
                                  mabs_c);
           FC.kap = fsel(chg, kc, FC.kap, FC.zero);

@@ -11,6 +11,9 @@ echo "smoke rc=$?" >> gpurun_out/${tag}_smoke.log
 cp profiles/traffic.json gpurun_out/${tag}_traffic.json
 bash tools/gpu_c4prof.sh $tag "C5 shell 16" "C4 dilate 1" "C4 dilate 4" "C4 dilate 16" "C4 dilate 64" "C3 dilate 8" \
   "C3 erode 8" "C2 shell 4" > gpurun_out/${tag}_prof.log 2>&1
+# complete per-op DRAM traffic from a light ncu pass (the --set full capture of the big ops stops early)
+bash tools/gpu_traffic.sh $tag "C5 shell 16" "C4 dilate 64" "C4 dilate 32" "C4 dilate 16" "C4 dilate 8" "C4 dilate 4" \
+  "C4 dilate 2" "C4 dilate 1" "C3 dilate 8" "C3 erode 8" "C2 dilate 4" "C2 erode 4" "C2 shell 4" > gpurun_out/${tag}_traffic_run.log 2>&1
 cp gpurun_out/${tag}_traffic.json profiles/traffic.json   # (this box's copy: the bench lines below read it)
 python bench.py --steps 5 --warmup 3 > gpurun_out/${tag}_bench_c5.json 2> gpurun_out/${tag}_bench_c5.err
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${tag}_bench_reference.json \
