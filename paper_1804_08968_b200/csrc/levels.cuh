@@ -105,8 +105,14 @@ struct LvArgs {
                            // issues on the FMA pipe; ptxas turns plain predicated moves into ALU selects)
 };
 
-constexpr int LV_T = 64;
-constexpr int LV_DC = 3;     // piece chunks (4 pieces each) per thread in the cp.async ring
+#ifndef LV_T_N
+#define LV_T_N 64
+#endif
+constexpr int LV_T = LV_T_N;
+#ifndef LV_DC_N
+#define LV_DC_N 3
+#endif
+constexpr int LV_DC = LV_DC_N;     // piece chunks (4 pieces each) per thread in the cp.async ring
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {   // dst: shared address
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
@@ -138,7 +144,7 @@ struct LvTab {
 };
 
 template <int LMAX>
-__global__ void __launch_bounds__(LV_T, 8) levels_kernel(LvArgs A) {
+__global__ void __launch_bounds__(LV_T, 512 / LV_T) levels_kernel(LvArgs A) {
   constexpr int NV = LvTab<LMAX>::NV, HS = LvTab<LMAX>::HS;
   __shared__ __align__(16) float Hs[257 * HS];   // h(kappa, k0 + k), NaN beyond R or out of reach;
                                                   // row R+1: all NaN (the "null piece")
