@@ -154,6 +154,7 @@ class Slab:
         inside every op.)"""
         if self.transport != "caller":
             return
+        check_slabs(self.ny, self.world, R)   # (a neighbour sends min(R, its rows): every slab needs R rows)
         nrows = self.y1 - self.y0
         send = min(R, nrows)
         lo = self.src.download_rows(0, send, device=True) if self.rank > 0 else None
@@ -162,6 +163,12 @@ class Slab:
         nhi = min(R, self.ny - self.y1)
         if self.world > 1:
             halo_lo, halo_hi = halo_exchange(lo, hi, self.rank, self.world, nlo, nhi, self.nx, group)
+            # the receives complete on torch's current stream; the library reads the buffers on the
+            # handle's own stream: order them (Work.wait() orders only torch's stream)
+            recv = halo_lo if halo_lo is not None else halo_hi
+            if recv is not None and recv[0].is_cuda:
+                import torch
+                torch.cuda.current_stream(recv[0].device).synchronize()
         else:
             halo_lo = halo_hi = None
         self.src.upload_halo(0, *(halo_lo if halo_lo is not None else (None, None)), nlo if halo_lo is not None else 0)
