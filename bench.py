@@ -207,12 +207,11 @@ def run_reference(a, rank, world):
     host = G.config(a.config)
     cores = host_cores()
     if a.op == "rasterize":   # the host generator dexelgen.c on the whole grid
-        _, zmin_w, zmax_w, sph, ssg, box, bsg = G.shape_config(a.config)
+        _, host_gen, _ = raster_job(a.config, G)
         ts = []
         for it in range(a.warmup + a.steps):
             t0 = time.perf_counter()
-            G.shapes(host.nx, host.ny, zmin_w, zmax_w, spheres=sph[ssg > 0], voids=sph[ssg < 0],
-                     boxes=box[bsg > 0], box_voids=box[bsg < 0], nthreads=cores)
+            host_gen(cores)
             if it >= a.warmup:
                 ts.append(time.perf_counter() - t0)
         tot = sum(ts)
@@ -246,6 +245,23 @@ def run_reference(a, rank, world):
             "cpu_baseline": {"value": v, "unit": "columns/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "columns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def raster_job(config, G, dx=None):
+    """rasterize of a config's solid: (GPU step on a grid, the host generator
+    dexelgen.c on the whole grid with `cores` threads, host->device bytes per GPU step).  C3 is
+    the noisy gyroid (dexel_rasterize_gyroid, its parameters only cross), the others the analytic
+    spheres and boxes (dexel_rasterize_shapes, the shape arrays cross)."""
+    if config == "C3":
+        n = G.CONFIGS["C3"]["n"]
+        gp = (64.0, 0.2, 0.05, G.SEED_BASE + 3)
+        return (lambda g: dx.dexel_rasterize_gyroid(g, 0.0, float(n), *gp),
+                lambda cores: G.gyroid(n, *gp, nthreads=cores), 6 * 8)
+    n, zmin_w, zmax_w, sph, ssg, box, bsg = G.shape_config(config)
+    return (lambda g: dx.dexel_rasterize_shapes(g, zmin_w, zmax_w, sph, ssg, box, bsg),
+            lambda cores: G.shapes(n, n, zmin_w, zmax_w, spheres=sph[ssg > 0], voids=sph[ssg < 0], boxes=box[bsg > 0],
+                                   box_voids=box[bsg < 0], nthreads=cores),
+            int(sph.nbytes + ssg.nbytes + box.nbytes + bsg.nbytes))
 
 
 # ------------------------------------------------------------------ algorithmic bytes
@@ -309,12 +325,12 @@ def run_b200(a, rank, world, local_rank):
     # rasterize: a step dexelises the config's analytic solid into the grid
     raster = a.op == "rasterize"
     if raster:
-        _, zmin_w, zmax_w, sph, ssg, box, bsg = G.shape_config(a.config)
+        gpu_gen, host_gen, raster_h2d = raster_job(a.config, G, dx)
     out_grid = src if raster else dst
 
     def step():
         if raster:
-            dx.dexel_rasterize_shapes(src, zmin_w, zmax_w, sph, ssg, box, bsg)
+            gpu_gen(src)
             return
         # (y-slabs: the op exchanges its R halo rows with ranks g-1 / g+1 over NCCL internally)
         slab.op(a.op, a.r)
@@ -415,7 +431,7 @@ def run_b200(a, rank, world, local_rank):
         torch.cuda.synchronize()
         e_ms = 1e3 * (time.perf_counter() - t0) / ke
         e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
-               "h2d_bytes_per_step": int(sph.nbytes + ssg.nbytes + box.nbytes + bsg.nbytes),
+               "h2d_bytes_per_step": raster_h2d,
                "d2h_bytes_per_step": 8 * (ncol + 1) + 8 * nout, "ms_per_step": e_ms}
     elif not a.no_e2e:
         # every rank: its slab's input CSR from pinned host memory, the (collective) op, its output
@@ -465,8 +481,7 @@ def run_b200(a, rank, world, local_rank):
     if not a.no_cpu and rank == 0 and world == 1 and raster:
         cores = host_cores()
         t0 = time.perf_counter()
-        G.shapes(host.nx, host.ny, zmin_w, zmax_w, spheres=sph[ssg > 0], voids=sph[ssg < 0], boxes=box[bsg > 0],
-                 box_voids=box[bsg < 0], nthreads=cores)
+        host_gen(cores)
         dt = time.perf_counter() - t0
         cpu = {"value": ncol / dt, "unit": "columns/s", "cores": cores, "kind": "oracle",
                "sample": f"the host generator dexelgen.c (fp64 per-column CSG, the definition the GPU path is "

@@ -174,6 +174,21 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
                                     const int32_t* sph_sign, int nbox, const double* box,
                                     const int32_t* box_sign, int src_on_device);
 
+/* GPU dexelisation of the noisy gyroid (BASELINE.json configs[2]; the
+ * implicit-solid case of PAPER.md:114-118 dexel buffers): g's rows := the solid
+ * F + eps - t > 0, F = sin X cos Y + sin Y cos Z + sin Z cos X, X = 2 pi x / period (same for
+ * Y, Z), column (i, j) at x = i + 1/2, y = j + 1/2 (global row j).  F + eps is sampled at
+ * z = zmin + m + 1/2, m = 0 .. zmax - zmin - 1, eps = amp (2u - 1) with u the counter generator's
+ * uniform (splitmix64 keyed by (seed, stream 6, column * nz + m)); endpoints are the linear roots
+ * between samples, the field held beyond the first / last sample.  Per column in fp64 without
+ * contraction (sin / cos from the host libm), clipped, shifted to the local frame, rounded to
+ * fp32 and canonicalised: bitwise the host generator (dexelgen.c dexelgen_gyroid).
+ *   zmin, zmax: integers, 0 <= zmin < zmax, giving the handle's frame (as dexel_rasterize_shapes);
+ *   period > 0, t finite, amp >= 0 (else DEXEL_EINVAL, grid unchanged).
+ * Two launches (count, scan, fill): no per-column capacity.  Synchronises the stream. */
+dexel_status dexel_rasterize_gyroid(dexel_grid g, double zmin, double zmax, double period, double t, double amp,
+                                    uint64_t seed);
+
 /* Attach halo rows (multi-GPU slabs): side 0 = the nrows global rows directly
  * below y0, side 1 = the nrows rows directly above y1 (row-major CSR of
  * nrows*nx columns, same conventions and validation as dexel_upload).  nrows

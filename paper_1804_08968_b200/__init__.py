@@ -24,7 +24,7 @@ _STATUS = {1: "EINVAL", 2: "ENOMEM", 3: "EMISMATCH", 4: "EOVERFLOW", 5: "ECUDA",
 
 # every symbol include/dexel.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel_shell", "dexel_open", "dexel_close",
-           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_trim_workspace", "dexel_size",
+           "dexel_dilate_slices", "dexel_erode_slices", "dexel_shell_slices", "dexel_rasterize_shapes", "dexel_rasterize_gyroid", "dexel_trim_workspace", "dexel_size",
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows", "dexel_nccl_unique_id", "dexel_nccl_comm_init", "dexel_nccl_comm_destroy",
@@ -84,6 +84,8 @@ def lib():
             "dexel_shell_slices": ([vp, ctypes.c_float, ctypes.c_float, vp], ctypes.c_int),
             "dexel_rasterize_shapes": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, ctypes.c_int, vp,
                                         vp, ctypes.c_int], ctypes.c_int),
+            "dexel_rasterize_gyroid": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, u64], ctypes.c_int),
             "dexel_trim_workspace": ([ctypes.c_int], ctypes.c_int),
             "dexel_size": ([vp, u64p], ctypes.c_int),
             "dexel_download": ([vp, vp, vp, u64, ctypes.c_int], ctypes.c_int),
@@ -343,6 +345,15 @@ def dexel_rasterize_shapes(g: Grid, zmin: float, zmax: float, sph=None, sph_sign
     _check(lib().dexel_rasterize_shapes(g.h, float(zmin), float(zmax), len(sph), sph.ctypes.data if len(sph) else None,
                                         ss.ctypes.data if len(ss) else None, len(box),
                                         box.ctypes.data if len(box) else None, bs.ctypes.data if len(bs) else None, 0))
+    return g
+
+
+def dexel_rasterize_gyroid(g: Grid, zmin: float, zmax: float, period: float = 64.0, t: float = 0.2,
+                           amp: float = 0.05, seed: int = 0) -> Grid:
+    """GPU dexelisation of the noisy gyroid (config C3): g := {F + eps > t} on g's
+    rows, bitwise the host generator dexelgen.gyroid with the same (period, t, amp, seed)."""
+    _check(lib().dexel_rasterize_gyroid(g.h, float(zmin), float(zmax), float(period), float(t), float(amp),
+                                        int(seed) & 0xFFFFFFFFFFFFFFFF))
     return g
 
 

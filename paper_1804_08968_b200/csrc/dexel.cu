@@ -1744,6 +1744,77 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   return DEXEL_OK;
 }
 
+dexel_status dexel_rasterize_gyroid(dexel_grid g, double zmin, double zmax, double period, double t, double amp,
+                                    uint64_t seed) {
+  g_err.clear();
+  if (!g) return fail(DEXEL_EINVAL, "NULL handle");
+  const double zref = 0.5 * (zmin + zmax);
+  if (!(zmin < zmax) || zref != g->d.z_ref || (float)(zmin - zref) != g->d.z_lo || (float)(zmax - zref) != g->d.z_hi)
+    return fail(DEXEL_EINVAL, "[zmin, zmax] must give the grid's frame: z_ref = (zmin + zmax)/2, "
+                              "z_lo = fl32(zmin - z_ref), z_hi = fl32(zmax - z_ref)");
+  if (!(zmin >= 0.0 && zmin == std::floor(zmin) && zmax == std::floor(zmax) && zmax - zmin <= (double)(1 << 24)))
+    return fail(DEXEL_EINVAL, "gyroid: zmin and zmax must be integers, 0 <= zmin < zmax (samples at zmin + m + 1/2)");
+  if (!(std::isfinite(period) && period > 0.0 && std::isfinite(t) && std::isfinite(amp) && amp >= 0.0))
+    return fail(DEXEL_EINVAL, "gyroid: period > 0, finite t and amp >= 0 required");
+  CK(cudaSetDevice(g->d.device));
+  const int nx = g->d.nx, nrows = g->nrows, y0 = g->d.y0, z0 = (int)zmin, nz = (int)(zmax - zmin);
+  // sin / cos of w (k + 1/2) from the host's libm -- the generator's own values (dexelgen.c)
+  const double w = 2.0 * M_PI / period;
+  const int nk = std::max({nx, g->d.ny, z0 + nz});
+  std::vector<double> tab(2 * (size_t)nk);
+  for (int k = 0; k < nk; ++k) {
+    tab[k] = std::sin(w * (k + 0.5));
+    tab[nk + k] = std::cos(w * (k + 0.5));
+  }
+  auto mix = [](uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  const uint64_t key = mix(mix(seed) ^ (6ULL * 0xD1B54A32D192ED03ULL));   // stream 6 (dexelgen_gyroid)
+  dexel_status s;
+  dexel_stats stats{};
+  Temps T(g, &stats);
+  const int64_t ncol = g->ncol;
+  double* dtab = nullptr;
+  uint32_t* cnt = nullptr;
+  if ((s = T.get(sizeof(double) * tab.size() + 16, (void**)&dtab))) return s;
+  if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&cnt))) return s;
+  CK(cudaMemcpyAsync(dtab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, g->stream));
+  GyroidArgs A{nx, nrows, y0, nz, z0, t, amp, zref, key, dtab, dtab + nk, cnt, nullptr, nullptr};
+  const unsigned blocks = (unsigned)((ncol + 255) / 256);
+  if (ncol > 0) LAUNCH(T, K_RASTER, gyroid_kernel<false><<<blocks, 256, 0, g->stream>>>(A));
+  CK(cudaGetLastError());
+  // offsets, then the endpoints (an error from here on leaves the grid empty)
+  if (!g->off.p && (s = dalloc(g, g->off, sizeof(uint64_t) * (ncol + 1)))) return s;
+  uint64_t n = 0;
+  if ((s = scan_counts(g, T, cnt, (uint64_t)ncol, (uint64_t*)g->off.p, &n))) {   // (synchronises: tab is read)
+    set_empty(g);
+    return s;
+  }
+  {
+    const size_t need = sizeof(float2) * (n + 1);
+    if (!(g->ep.p && g->ep.bytes >= need && g->ep.bytes - need <= need / 4)) {
+      dfree(g, g->ep);
+      if ((s = dalloc(g, g->ep, need))) {
+        set_empty(g);
+        return s;
+      }
+    }
+  }
+  A.off = (const uint64_t*)g->off.p;
+  A.ep = (float2*)g->ep.p;
+  if (ncol > 0) LAUNCH(T, K_RASTER, gyroid_kernel<true><<<blocks, 256, 0, g->stream>>>(A));
+  CK(cudaGetLastError());
+  T.prof.finish();
+  CK(timed_sync(g->stream));
+  g->n = n;
+  stats.n_out = n;
+  g->stats = stats;
+  return DEXEL_OK;
+}
+
 dexel_status dexel_pass1(dexel_grid g, float r, int complement, uint64_t* offsets, float* z, uint8_t* kappa,
                          uint64_t cap, uint64_t* n_pieces, int on_dev) {
   g_err.clear();

@@ -217,4 +217,87 @@ __global__ void raster_bin_fill(RasterBin B, const uint64_t* __restrict__ off, u
     }
 }
 
+// ---- the noisy gyroid of config C3 (BASELINE.json configs[2]; SURVEY 8(f) NEXT #3's implicit
+// solid): F = sin X cos Y + sin Y cos Z + sin Z cos X, X = 2 pi x / period (same for Y, Z), solid
+// where F + eps - t > 0.  F + eps is sampled at z = zmin + m + 1/2 (m = 0 .. nz - 1) with eps =
+// amp (2u - 1), u uniform from the counter generator (splitmix64 of key ^ (column * nz + m)),
+// linearly interpolated in z; endpoints are the linear roots between samples; beyond the first /
+// last sample the field is held (the column's first interval may start at zmin, its last end at
+// zmax).  Exactly the host generator's arithmetic (dexelgen.c, dexelgen_gyroid), in fp64 without
+// contraction: the sin / cos values come from the host's libm as tables (sn / cs[k] =
+// sin / cos(w (k + 1/2))), so the CSR is bitwise the host's.
+// One thread per column, two launches: count (FILL = false) and, after the scan, fill.
+struct GyroidArgs {
+  int nx, nrows, y0, nz, z0;    // columns, local rows (global y0 + jl), samples, integral zmin
+  double t, amp, zref;
+  uint64_t key;                 // mix64(mix64(seed) ^ stream 6 * K): the generator's per-stream key
+  const double* sn;             // [max(nx, y0 + nrows, z0 + nz)]
+  const double* cs;
+  uint32_t* cnt;                // [ncol] (count launch)
+  const uint64_t* off;          // [ncol + 1] (fill launch)
+  float2* ep;
+};
+
+__device__ __forceinline__ uint64_t gy_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(256) gyroid_kernel(GyroidArgs A) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)A.nrows * A.nx) return;
+  const int i = (int)(c % A.nx), j = A.y0 + (int)(c / A.nx);
+  const double sx = A.sn[i], cx = A.cs[i], sy = A.sn[j], cy = A.cs[j];
+  const uint64_t col = (uint64_t)j * (uint64_t)A.nx + (uint64_t)i;
+  const double zmin = (double)A.z0, zmax = (double)(A.z0 + A.nz);
+  auto field = [&](int m) {
+    const double u = (double)(gy_mix64(A.key ^ (col * (uint64_t)A.nz + (uint64_t)m)) >> 11) * (1.0 / 9007199254740992.0);
+    const double eps = __dmul_rn(A.amp, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+    const double sz = A.sn[A.z0 + m], cz = A.cs[A.z0 + m];
+    const double f = __dadd_rn(__dadd_rn(__dmul_rn(sx, cy), __dmul_rn(sy, cz)), __dmul_rn(sz, cx));
+    return __dsub_rn(__dadd_rn(f, eps), A.t);
+  };
+  uint32_t k = 0;
+  float la = 0.f, lb = 0.f;   // last output interval (merge target)
+  float2* out = FILL ? A.ep + A.off[c] : nullptr;
+  // clip, shift to the local frame, round to fp32, canonicalise (dexelgen.c finish_column)
+  auto emit = [&](double dlo, double dhi) {
+    const double clo = dlo < zmin ? zmin : dlo;
+    const double chi = dhi > zmax ? zmax : dhi;
+    if (!(clo < chi)) return;
+    const float a = (float)__dsub_rn(clo, A.zref), b = (float)__dsub_rn(chi, A.zref);
+    if (k > 0 && a <= lb) {
+      if (b > lb) {
+        lb = b;
+        if (FILL) out[k - 1] = make_float2(la, lb);
+      }
+      return;
+    }
+    if (!(a < b)) return;
+    la = a;
+    lb = b;
+    if (FILL) out[k] = make_float2(a, b);
+    ++k;
+  };
+  double f0 = field(0);
+  bool inside = f0 > 0.0;
+  double start = zmin;
+  for (int m = 0; m + 1 < A.nz; ++m) {
+    const double f1 = field(m + 1);
+    const bool nin = f1 > 0.0;
+    if (nin != inside) {
+      const double zc = __dadd_rn(__dadd_rn((double)(A.z0 + m), 0.5), __ddiv_rn(f0, __dsub_rn(f0, f1)));
+      if (nin) start = zc;
+      else emit(start, zc);
+      inside = nin;
+    }
+    f0 = f1;
+  }
+  if (inside) emit(start, zmax);
+  if (!FILL) A.cnt[c] = k;
+}
+
 }  // namespace dexel

@@ -650,6 +650,43 @@ def test_rasterize_shapes_errors(dx):
     g.close()
 
 
+@pytest.mark.parametrize("n,period,t,amp,seed", [(1024, 64.0, 0.2, 0.05, G.SEED_BASE + 3),   # C3 itself
+                                                  (37, 16.0, 0.2, 0.05, 7), (64, 12.5, -0.3, 0.4, 11),
+                                                  (50, 24.0, 0.0, 0.0, 3), (33, 64.0, 2.0, 0.05, 5)])
+def test_rasterize_gyroid_bitwise_host_generator(dx, n, period, t, amp, seed):
+    """dexel_rasterize_gyroid gives bitwise the CSR of the host generator's noisy gyroid
+    (dexelgen.c, fp64 samples + linear roots): C3 at full size, small grids with other periods,
+    thresholds (t = 2: the empty solid), noise off and strong noise (many short intervals)."""
+    host = G.gyroid(n, period, t, amp, seed)
+    g = dx.Grid(n, n, host.z_lo, host.z_hi, host.z_ref)
+    dx.dexel_rasterize_gyroid(g, 0.0, float(n), period, t, amp, seed)
+    off, ep = g.download()
+    assert np.array_equal(off.astype(np.uint64), host.off.astype(np.uint64))
+    assert np.array_equal(ep, host.ep)
+    g.close()
+
+
+def test_rasterize_gyroid_slab_and_errors(dx):
+    """A y-slab handle gets the host's rows [y0, y1); invalid arguments leave the grid unchanged."""
+    n = 96
+    host = G.gyroid(n, 20.0, 0.1, 0.1, 99)
+    y0, y1 = 40, 71
+    g = dx.Grid(n, n, host.z_lo, host.z_hi, host.z_ref, 1.0, 0, None, y0, y1, 1, 3)
+    dx.dexel_rasterize_gyroid(g, 0.0, float(n), 20.0, 0.1, 0.1, 99)
+    off, ep = g.download()
+    a, b = int(host.off[y0 * n]), int(host.off[y1 * n])
+    assert np.array_equal(off.astype(np.int64), host.off[y0 * n:y1 * n + 1].astype(np.int64) - a)
+    assert np.array_equal(ep, host.ep[2 * a:2 * b])
+    before = g.download()
+    for args in [(0.0, 48.0, 20.0, 0.1, 0.1, 1), (0.0, float(n), 0.0, 0.1, 0.1, 1),
+                 (0.0, float(n), 20.0, 0.1, -1.0, 1)]:
+        with pytest.raises(Exception):
+            dx.dexel_rasterize_gyroid(g, *args)
+        after = g.download()
+        assert np.array_equal(before[0], after[0]) and np.array_equal(before[1], after[1])
+    g.close()
+
+
 # ---------------------------------------------------------------- tri-dexel offsets (NEXT #4)
 @pytest.mark.parametrize("cfg,op,r", [("C1", "dilate", 3.0), ("C2", "shell", 4.0), ("C2", "erode", 4.0)])
 def test_tridexel_buffers_match_oracle(dx, cfg, op, r):
