@@ -103,6 +103,14 @@ struct dexel_grid_s {
     std::vector<float> host;
   } htab[2];
   int htab_next = 0;
+  // small-temporary arena (below WS_MIN): an op's small temporaries are carved from one block kept
+  // on the handle between ops (stream-ordered reuse: the handle's ops run on its stream), instead
+  // of a cudaMallocAsync / cudaFreeAsync pair each -- a dozen per op, a large share of a small
+  // op's host time.  Temps nest as a stack (mark / reset); a request that does not fit falls back
+  // to its own allocation and grows the arena for the next op.
+  Buf arena;
+  size_t arena_top = 0, arena_want = 0;
+  int arena_depth = 0;
 };
 
 namespace {
@@ -260,15 +268,28 @@ struct Temps {
   std::vector<Buf> bufs;
   std::vector<int> wsi;   // workspace entries this op holds
   Prof prof;
+  size_t mark = 0, top = 0;   // the handle's arena: this op's first byte, its next free byte
   explicit Temps(dexel_grid g_, dexel_stats* st = nullptr) : g(g_) {
     prof.st = g_->stream;
     prof.s = st;
     prof.on = g_timing && st != nullptr;
+    if (g->arena_depth == 0 && g->arena_want > g->arena.bytes) {   // grow (no op holds it now)
+      dfree(g, g->arena);
+      if (dalloc(g, g->arena, g->arena_want + g->arena_want / 4 + ((size_t)64 << 10)) != DEXEL_OK) {
+        g->arena = Buf{};
+        g_err.clear();
+      }
+    }
+    ++g->arena_depth;
+    mark = top = g->arena_top;
   }
   ~Temps() {
     prof.finish();
     for (auto& b : bufs) dfree(g, b);
     while (!wsi.empty()) release_ws(0);
+    g->arena_want = std::max(g->arena_want, top);
+    g->arena_top = mark;
+    --g->arena_depth;
   }
   void release_ws(size_t t) {   // hand block wsi[t] back, ordered after this op's stream work
     DevWs& W = dev_ws(g->d.device);
@@ -316,6 +337,16 @@ struct Temps {
       *p = b.p;
       return DEXEL_OK;
     }
+    const size_t a = (bytes + 255) & ~(size_t)255;
+    if (top + a <= ((size_t)256 << 20)) {   // (the arena holds at most 256 MB)
+      const size_t at = top;
+      top += a;
+      if (g->arena.p && g->arena_top == at && top <= g->arena.bytes) {   // (innermost Temps only)
+        g->arena_top = top;
+        *p = (char*)g->arena.p + at;
+        return DEXEL_OK;
+      }
+    }
     Buf b;
     dexel_status s = dalloc(g, b, bytes);
     if (s) return s;
@@ -323,7 +354,7 @@ struct Temps {
     *p = b.p;
     return DEXEL_OK;
   }
-  void release(void* p) {
+  void release(void* p) {   // (an arena block is released with its Temps)
     for (auto& b : bufs)
       if (b.p == p) dfree(g, b);
     for (size_t t = 0; t < wsi.size(); ++t) {
@@ -1900,6 +1931,7 @@ void dexel_destroy(dexel_grid g) {
   dfree(g, g->spare_off);
   dfree(g, g->spare_ep);
   dfree(g, g->hdr);
+  dfree(g, g->arena);
   for (auto& H : g->htab) dfree(g, H.dev);
   if (g->comm) {
     cudaStreamSynchronize(g->comm);

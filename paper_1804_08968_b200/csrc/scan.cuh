@@ -105,4 +105,79 @@ __global__ void scan_tiles_write(const uint32_t* __restrict__ cnt, uint64_t n, c
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
 }
 
+// ---- single-launch variant: decoupled look-back (each tile publishes its aggregate, then its
+// inclusive prefix, in a status word; a tile's thread 0 walks back over its predecessors'
+// words).  Tiles take their index from an atomic ticket, so a tile only ever waits on tiles that
+// started before it (no deadlock whatever the block scheduling).  status[0 .. ntiles) and the
+// ticket (status[ntiles]) must be zero at launch.  Word: bits 62-63 = state (0 not ready,
+// 1 aggregate, 2 inclusive prefix), bits 0-61 = the value.
+constexpr unsigned long long SCAN_ST_A = 1ull << 62, SCAN_ST_P = 2ull << 62, SCAN_ST_V = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_lookback(const uint32_t* __restrict__ cnt, uint64_t n,
+                                                             unsigned long long* status, uint64_t* __restrict__ out) {
+  __shared__ uint32_t tile[SCAN_TILE];
+  __shared__ uint64_t res[SCAN_TILE];
+  __shared__ unsigned long long tid_s, prefix_s;
+  const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (threadIdx.x == 0) tid_s = atomicAdd(status + ntiles, 1ull);
+  __syncthreads();
+  const uint64_t t = tid_s;
+  const uint64_t base = t * SCAN_TILE;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    const uint64_t idx = base + (uint64_t)k * SCAN_THREADS + threadIdx.x;   // coalesced
+    tile[k * SCAN_THREADS + threadIdx.x] = idx < n ? cnt[idx] : 0u;
+  }
+  __syncthreads();
+  uint32_t v[SCAN_ITEMS];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = tile[threadIdx.x * SCAN_ITEMS + k];
+    sum += v[k];
+  }
+  uint64_t total;
+  uint64_t ex = block_excl_scan_u64(sum, &total);
+  if (threadIdx.x == 0) {
+    unsigned long long excl = 0;
+    if (t == 0) {
+      st_release_u64(status, SCAN_ST_P | total);
+    } else {
+      st_release_u64(status + t, SCAN_ST_A | total);
+      for (int64_t q = (int64_t)t - 1;;) {
+        const unsigned long long w = ld_acquire_u64(status + q);
+        if (!(w & ~SCAN_ST_V)) continue;   // not ready yet: spin
+        excl += w & SCAN_ST_V;
+        if (w & SCAN_ST_P) break;
+        --q;
+      }
+      st_release_u64(status + t, SCAN_ST_P | (excl + total));
+    }
+    prefix_s = excl;
+  }
+  __syncthreads();
+  ex += prefix_s;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    res[threadIdx.x * SCAN_ITEMS + k] = ex;
+    ex += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    const uint64_t idx = base + (uint64_t)k * SCAN_THREADS + threadIdx.x;   // coalesced
+    if (idx < n) out[idx] = res[k * SCAN_THREADS + threadIdx.x];
+  }
+  if (t == ntiles - 1 && threadIdx.x == 0) out[n] = prefix_s + total;
+}
+
 }  // namespace dexel
