@@ -398,21 +398,19 @@ dexel_status scan_counts(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n
   return DEXEL_OK;
 }
 
-// exclusive scan of cnt[0..n) into off[0..n], the total at off[n] (stays on the device)
-dexel_status scan_counts_dev(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n, uint64_t* off) {
+// exclusive scan of cnt[0..n) into off[0..n], the total at off[n] (stays on the device): one
+// decoupled look-back launch (scan.cuh) whose status words -- scan_status_words(n), zeroed by
+// the caller (the op zeroes them with its flag words) -- live at `status`
+inline size_t scan_status_words(uint64_t n) { return (size_t)((n + SCAN_TILE - 1) / SCAN_TILE) + 1; }
+dexel_status scan_counts_dev(dexel_grid g, Temps& T, const uint32_t* cnt, uint64_t n, uint64_t* off,
+                             unsigned long long* status) {
   const uint64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (n == 0) {
     CK(cudaMemsetAsync(off, 0, sizeof(uint64_t), g->stream));
     return DEXEL_OK;
   }
-  uint64_t* sums = nullptr;
-  dexel_status s = T.get(sizeof(uint64_t) * (ntiles + 2), (void**)&sums);
-  if (s) return s;
-  LAUNCH(T, K_SCAN, scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums));
-  LAUNCH(T, K_SCAN, scan_sums_exclusive<<<1, SCAN_THREADS, 0, g->stream>>>(sums, ntiles));
-  LAUNCH(T, K_SCAN, scan_tiles_write<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, sums, off));
+  LAUNCH(T, K_SCAN, scan_lookback<<<(unsigned)ntiles, SCAN_THREADS, 0, g->stream>>>(cnt, n, status, off));
   CK(cudaGetLastError());
-  T.release(sums);
   return DEXEL_OK;
 }
 
@@ -1117,7 +1115,9 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   uint32_t* ocnt = nullptr;
   unsigned* opf = nullptr;   // the op's flag words and statistics (kernels.cuh OpFlag)
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&ocnt))) return s;
-  if ((s = T.get(sizeof(unsigned) * OPF_WORDS, (void**)&opf))) return s;
+  // the op's flag words, then the output scan's look-back status words: one memset per attempt
+  const size_t opf_bytes = sizeof(unsigned) * OPF_WORDS + sizeof(unsigned long long) * scan_status_words((uint64_t)ncol);
+  if ((s = T.get(opf_bytes, (void**)&opf))) return s;
   int acc = src->p2_acc > 0 ? src->p2_acc : 32;
   float2* stage = nullptr;
   // Every capacity of the op (piece slots and arena, level slots and arena, the pass-2
@@ -1132,7 +1132,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
     if (pass2_smem_bytes(op, acc, 32) > P2_SMEM_MAX &&
         (s = T.get(sizeof(float2) * (size_t)(acc + 2) * band * nx + 16, (void**)&gacc)))
       return s;
-    CK(cudaMemsetAsync(opf, 0, sizeof(unsigned) * OPF_WORDS, st));
+    CK(cudaMemsetAsync(opf, 0, opf_bytes, st));
     uint32_t lev_cap_used = 0;
     for (int b0 = 0; b0 < src->nrows; b0 += band) {
       const int b1 = std::min(src->nrows, b0 + band);
@@ -1168,7 +1168,9 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
     // (when the total fits it: the kernel checks on the device)
     dst->n = 0;   // (from here on dst is being replaced: an error leaves it empty, run_op)
     if (!dst->off.p && (s = dalloc(dst, dst->off, sizeof(uint64_t) * (dst->ncol + 1)))) return s;
-    if ((s = scan_counts_dev(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p))) return s;
+    if ((s = scan_counts_dev(src, T, ocnt, (uint64_t)ncol, (uint64_t*)dst->off.p,
+                             reinterpret_cast<unsigned long long*>(opf + OPF_WORDS))))
+      return s;
     if (!dst->ep.p && (s = dalloc(dst, dst->ep, sizeof(float2) * (size_t)(2 * src->n + 1024)))) return s;
     const uint64_t ep_cap = dst->ep.bytes / sizeof(float2);
     if (ncol > 0)

@@ -19,6 +19,9 @@ python bench.py --steps 5 --warmup 3 > gpurun_out/${tag}_bench_c5.json 2> gpurun
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${tag}_bench_reference.json \
   2> gpurun_out/${tag}_bench_reference.err
 bash tools/bench_matrix.sh $tag $steps
+# GPU dexelisation lines: shapes (C2, C4, C5) and the noisy gyroid (C3)
+for c in C2 C3 C4 C5; do timeout 900 python bench.py --config $c --op rasterize --steps 5 --warmup 3; done \
+  > gpurun_out/${tag}_raster.jsonl 2> gpurun_out/${tag}_raster.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${tag}_launches.log 2>&1
 timeout 300 python bench.py --gpus 2 --steps 2 --warmup 3 > gpurun_out/${tag}_gpus2.log 2>&1
