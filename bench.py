@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--r", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-slabs", type=int, default=8,
+                    help="y-slabs of the streamed host-to-host op (dexel_pipe_run) the e2e number is measured "
+                         "with at N=1; 0: only the serial upload + op + download")
     ap.add_argument("--cpu-rows", type=int, default=None, help="rows in the oracle band sample")
     a = ap.parse_args()
     a.op = a.op or DEFAULT_OP[a.config]
@@ -474,7 +477,35 @@ def run_b200(a, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             e_ms, byts = float(tm.item()), [int(v) for v in t[1:].tolist()]
         e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
-               "h2d_bytes_per_step": byts[0], "d2h_bytes_per_step": byts[1], "ms_per_step": e_ms}
+               "h2d_bytes_per_step": byts[0], "d2h_bytes_per_step": byts[1], "ms_per_step": e_ms,
+               "api": "dexel_upload + op + dexel_download (serial)"}
+        if world == 1 and a.e2e_slabs > 0 and a.op in ("dilate", "erode", "shell"):
+            # the streamed host-to-host call (dexel_pipe_run): the same pinned host CSRs, cut into
+            # y-slabs so the upload of slab q+1, the op on slab q and the download of slab q-1 overlap;
+            # each slab also uploads its R halo rows per side (counted in h2d_bytes_per_step)
+            ns = min(a.e2e_slabs, host.ny)
+            pipe = dx.Pipe(host.nx, host.ny, host.z_lo, host.z_hi, ns, getattr(host, "z_ref", 0.0),
+                           getattr(host, "spacing", 1.0), dev)
+            r_b = a.r if a.op == "shell" else 0.0
+            hal = 0
+            for q in range(ns):
+                y0, y1 = host.ny * q // ns, host.ny * (q + 1) // ns
+                for lo, hi in ((max(0, y0 - R), y0), (y1, min(host.ny, y1 + R))):
+                    if hi > lo:
+                        hal += 8 * ((hi - lo) * host.nx + 1) + 8 * int(host.off[hi * host.nx] - host.off[lo * host.nx])
+            pipe.run(a.op, a.r, r_b, h_off, h_ep, o_off, o_ep)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(ke):
+                nout_p = pipe.run(a.op, a.r, r_b, h_off, h_ep, o_off, o_ep)
+            p_ms = 1e3 * (time.perf_counter() - t0) / ke     # (the call returns when the host CSR is complete)
+            pipe.close()
+            assert nout_p == nout, (nout_p, nout)
+            serial = e2e
+            e2e = {"value": ncol / (p_ms / 1e3), "unit": "columns/s",
+                   "h2d_bytes_per_step": byts[0] + hal + 8 * (ns - 1), "d2h_bytes_per_step": byts[1] + 8 * (ns - 1),
+                   "ms_per_step": p_ms, "api": f"dexel_pipe_run, {ns} y-slabs (upload / op / download overlapped)",
+                   "serial": serial}
 
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None

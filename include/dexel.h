@@ -231,6 +231,30 @@ void dexel_destroy(dexel_grid g);
 /* Thread-local description of the last error ("" if none). */
 const char* dexel_last_error(void);
 
+/* Host-to-host ops, streamed in y-slabs ("the 2D dilations can be performed
+ * completely independently in every slice", so rows [y0, y1) of the result need only input rows
+ * [y0 - R, y1 + R)).  A pipeline cuts the grid into nslabs row slabs, each with its own pair of
+ * device handles and its own stream; dexel_pipe_run uploads slab q+1 (its rows plus R halo rows
+ * on each side, straight from the host CSR), runs the op on slab q (the same kernels as
+ * dexel_dilate / dexel_erode / dexel_shell, caller-managed halo mode) and downloads the result
+ * of slab q-1 at the same time, on three host threads.  The result is bitwise the one
+ * dexel_upload + op + dexel_download of the whole grid gives.
+ *   d:         the whole grid on one device (nranks 1, y0 0, y1 ny, nccl_comm NULL; d->stream unused)
+ *   nslabs:    1..ny (1: no overlap; the slabs' rows are ny*q/nslabs .. ny*(q+1)/nslabs)
+ *   op:        0 dilate (r_a), 1 erode (r_a), 2 shell (r_a = r_out, r_b = r_in)
+ *   offsets, endpoints: HOST canonical CSR of the whole grid (nx*ny + 1 offsets from 0; pinned memory
+ *              lets the copies overlap the kernels, pageable memory works but serialises them)
+ *   out_offsets: HOST uint64[nx*ny + 1]; out_endpoints: HOST float[2*capacity]
+ *   *n_out:    the result's intervals; capacity < that -> DEXEL_EOVERFLOW (outputs partly written)
+ * Input validation and error codes as dexel_upload / the ops; on error the outputs are undefined.
+ * A pipeline is not re-entrant; it returns when the outputs are complete (no stream to wait on). */
+typedef struct dexel_pipe_s* dexel_pipe;
+dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out);
+dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const uint64_t* offsets,
+                            const float* endpoints, uint64_t* out_offsets, float* out_endpoints,
+                            uint64_t capacity, uint64_t* n_out);
+void dexel_pipe_destroy(dexel_pipe p);   /* NULL-safe */
+
 /* Route device allocations through a caller allocator (e.g. the PyTorch
  * caching allocator).  NULL,NULL restores cudaMallocAsync/cudaFreeAsync.
  * Each buffer is released by the allocator that produced it, so the hook may

@@ -28,7 +28,7 @@ EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows", "dexel_nccl_unique_id", "dexel_nccl_comm_init", "dexel_nccl_comm_destroy",
-           "dexel_link_slabs"]
+           "dexel_link_slabs", "dexel_pipe_create", "dexel_pipe_run", "dexel_pipe_destroy"]
 
 
 class DexelError(RuntimeError):
@@ -102,6 +102,10 @@ def lib():
             "dexel_nccl_comm_init": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
             "dexel_nccl_comm_destroy": ([vp], ctypes.c_int),
             "dexel_link_slabs": ([ctypes.POINTER(vp), ctypes.c_int], ctypes.c_int),
+            "dexel_pipe_create": ([ctypes.POINTER(dexel_desc), ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+            "dexel_pipe_run": ([vp, ctypes.c_int, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp, u64, u64p],
+                               ctypes.c_int),
+            "dexel_pipe_destroy": ([vp], None),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -259,6 +263,39 @@ class Grid:
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
             lib().dexel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class Pipe:
+    """Host-to-host ops streamed in y-slabs (dexel_pipe_*): upload, op and download overlap."""
+
+    OPS = {"dilate": 0, "erode": 1, "shell": 2}
+
+    def __init__(self, nx: int, ny: int, z_lo: float, z_hi: float, nslabs: int = 4, z_ref: float = 0.0,
+                 spacing: float = 1.0, device: int = 0):
+        self.desc = dexel_desc(nx, ny, spacing, z_ref, z_lo, z_hi, device, None, None, 0, 1, 0, ny)
+        h = ctypes.c_void_p()
+        _check(lib().dexel_pipe_create(ctypes.byref(self.desc), nslabs, ctypes.byref(h)))
+        self.h = h
+
+    def run(self, op: str, r_a: float, r_b: float, off, ep, out_off, out_ep) -> int:
+        """host CSR (off, ep) -> host CSR written into (out_off, out_ep); returns the interval count.
+        Arrays are numpy or CPU torch tensors (uint64/int64 offsets, float32 endpoints)."""
+        cap = (out_ep.size if isinstance(out_ep, np.ndarray) else out_ep.numel()) // 2
+        n = ctypes.c_uint64()
+        _check(lib().dexel_pipe_run(self.h, self.OPS[op], r_a, r_b, _ptr(off), _ptr(ep), _ptr(out_off),
+                                    _ptr(out_ep), cap, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().dexel_pipe_destroy(self.h)
             self.h = None
 
     def __del__(self):

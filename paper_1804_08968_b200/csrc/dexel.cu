@@ -16,7 +16,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -122,7 +124,7 @@ __global__ void rebase_offsets(const uint64_t* __restrict__ src, uint64_t n, uin
 }
 
 // host-side diagnostics (DEXEL_DEBUG): seconds spent in allocation calls and stream syncs
-double g_t_alloc = 0.0, g_t_sync = 0.0, g_t_free = 0.0, g_t_info = 0.0;
+thread_local double g_t_alloc = 0.0, g_t_sync = 0.0, g_t_free = 0.0, g_t_info = 0.0;   // (diagnostics of the calling thread's op)
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -1433,7 +1435,8 @@ dexel_status take_or_alloc(dexel_grid g, Buf* spare, Buf& b, size_t bytes) {
 }
 
 dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoints, int64_t ncol, uint64_t n,
-                      int on_dev, Buf* off_out, Buf* ep_out, Buf* spare_off = nullptr, Buf* spare_ep = nullptr) {
+                      int on_dev, Buf* off_out, Buf* ep_out, Buf* spare_off = nullptr, Buf* spare_ep = nullptr,
+                      bool sliced = false) {
   if (!offsets || (n > 0 && !endpoints)) return fail(DEXEL_EINVAL, "NULL argument");
   CK(cudaSetDevice(g->d.device));
   uint64_t first = 0, last = 0;
@@ -1445,7 +1448,10 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
     first = offsets[0];
     last = offsets[ncol];
   }
-  if (first != 0 || last != n) return fail(DEXEL_EINVAL, "offsets[0] must be 0 and offsets[ncols] == n_intervals");
+  // sliced (dexel_pipe_run): the rows are a slice of a larger CSR -- offsets[0] = b, `endpoints` points at
+  // interval b, and the device copy of the offsets is rebased to 0 before validation
+  if (sliced ? (last < first || last - first != n) : (first != 0 || last != n))
+    return fail(DEXEL_EINVAL, "offsets[0] must be 0 and offsets[ncols] == n_intervals");
   Buf off, ep;
   dexel_status s;
   if ((s = take_or_alloc(g, spare_off, off, sizeof(uint64_t) * (ncol + 1)))) return s;
@@ -1456,6 +1462,8 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
   const cudaMemcpyKind k = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   CK(cudaMemcpyAsync(off.p, offsets, sizeof(uint64_t) * (ncol + 1), k, g->stream));
   if (n) CK(cudaMemcpyAsync(ep.p, endpoints, sizeof(float) * 2 * n, k, g->stream));
+  if (sliced && first != 0)
+    rebase_kernel<<<(unsigned)((ncol + 1 + 255) / 256), 256, 0, g->stream>>>((uint64_t*)off.p, ncol + 1, first);
   Temps T(g);
   unsigned long long* bad = nullptr;
   if ((s = T.get(sizeof(unsigned long long), (void**)&bad))) {
@@ -1488,14 +1496,25 @@ dexel_status load_csr(dexel_grid g, const uint64_t* offsets, const float* endpoi
 
 extern "C" {
 
+static dexel_status upload_impl(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev,
+                                bool sliced);
+static dexel_status upload_halo_impl(dexel_grid g, int side, const uint64_t* offsets, const float* endpoints,
+                                     int nrows, uint64_t n, int on_dev, bool sliced);
+
 dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev) {
+  return upload_impl(g, offsets, endpoints, n, on_dev, false);
+}
+
+static dexel_status upload_impl(dexel_grid g, const uint64_t* offsets, const float* endpoints, uint64_t n, int on_dev,
+                                bool sliced) {
   g_err.clear();
   if (!g) return fail(DEXEL_EINVAL, "NULL handle");
   static const bool dbg = std::getenv("DEXEL_DEBUG") != nullptr;
   const double t0 = now_s();
   g_t_alloc = g_t_sync = 0.0;
   Buf off, ep;
-  dexel_status s = load_csr(g, offsets, endpoints, g->ncol, n, on_dev, &off, &ep, &g->spare_off, &g->spare_ep);
+  dexel_status s = load_csr(g, offsets, endpoints, g->ncol, n, on_dev, &off, &ep, &g->spare_off, &g->spare_ep,
+                            sliced);
   if (s) return s;
   if (dbg)
     std::fprintf(stderr, "[dexel] upload %llu intervals: %.2f ms (allocation calls %.2f ms, stream syncs %.2f ms)\n",
@@ -1513,6 +1532,11 @@ dexel_status dexel_upload(dexel_grid g, const uint64_t* offsets, const float* en
 
 dexel_status dexel_upload_halo(dexel_grid g, int side, const uint64_t* offsets, const float* endpoints, int nrows,
                                uint64_t n, int on_dev) {
+  return upload_halo_impl(g, side, offsets, endpoints, nrows, n, on_dev, false);
+}
+
+static dexel_status upload_halo_impl(dexel_grid g, int side, const uint64_t* offsets, const float* endpoints,
+                                     int nrows, uint64_t n, int on_dev, bool sliced) {
   g_err.clear();
   if (!g || (side != 0 && side != 1) || nrows < 0) return fail(DEXEL_EINVAL, "bad halo arguments");
   const int avail = side == 0 ? g->d.y0 : g->d.ny - g->d.y1;
@@ -1523,7 +1547,8 @@ dexel_status dexel_upload_halo(dexel_grid g, int side, const uint64_t* offsets, 
   g->hn[side] = 0;
   if (nrows == 0) return DEXEL_OK;
   Buf off, ep;
-  dexel_status s = load_csr(g, offsets, endpoints, (int64_t)nrows * g->d.nx, n, on_dev, &off, &ep);
+  dexel_status s = load_csr(g, offsets, endpoints, (int64_t)nrows * g->d.nx, n, on_dev, &off, &ep, nullptr, nullptr,
+                            sliced);
   if (s) return s;
   g->hoff[side] = off;
   g->hep[side] = ep;
@@ -2036,6 +2061,178 @@ dexel_status dexel_link_slabs(dexel_grid* slabs, int n) {
     slabs[q]->link[0] = q > 0 ? slabs[q - 1] : nullptr;
     slabs[q]->link[1] = q + 1 < n ? slabs[q + 1] : nullptr;
   }
+  return DEXEL_OK;
+}
+
+// ------------------------------------------------------------------ host pipeline
+// dexel_pipe: one op from a host CSR to a host CSR, streamed in y-slabs (dexel.h).  The host holds
+// every row, so each slab's halo rows are uploaded straight from the host CSR (caller-managed halo
+// mode: no exchange); three host threads keep the copy engines and the SMs busy at once:
+//   uploader   slab q+1: rows and halo rows host -> device (offsets rebased on the device), validation
+//   caller     slab q:   the op (pass 1, levels, pass 2: the same kernels as dexel_dilate/erode/shell)
+//   downloader slab q-1: result device -> host at its place in the output CSR, offsets shifted by the
+//                        intervals of the slabs before it
+// Each slab has its own stream; the stages hand slabs over under one mutex.
+struct dexel_pipe_s {
+  dexel_desc d;
+  int nslabs = 0;
+  std::vector<dexel_grid> src, dst;
+};
+
+namespace {
+struct PipeSync {
+  std::mutex mu;
+  std::condition_variable cv;
+  int uploaded = 0, computed = 0;   // slabs that left each stage
+  dexel_status err = DEXEL_OK;
+  std::string msg;
+  void fail_with(dexel_status s) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (err == DEXEL_OK) {
+      err = s;
+      msg = g_err;
+    }
+    cv.notify_all();
+  }
+};
+}  // namespace
+
+dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out) {
+  g_err.clear();
+  if (!d || !out) return fail(DEXEL_EINVAL, "NULL argument");
+  if (d->nranks != 1 || d->y0 != 0 || d->y1 != d->ny || d->nccl_comm)
+    return fail(DEXEL_EINVAL, "the pipeline's descriptor must describe the whole grid on one device");
+  if (nslabs < 1 || nslabs > d->ny) return fail(DEXEL_EINVAL, "nslabs must be in [1, ny]");
+  dexel_pipe p = new dexel_pipe_s();
+  p->d = *d;
+  p->nslabs = nslabs;
+  for (int q = 0; q < nslabs; ++q) {
+    dexel_desc dq = *d;
+    dq.stream = nullptr;   // a stream per slab (the stages overlap across slabs)
+    dq.rank = q;
+    dq.nranks = nslabs;
+    dq.y0 = (int)((int64_t)d->ny * q / nslabs);
+    dq.y1 = (int)((int64_t)d->ny * (q + 1) / nslabs);
+    dexel_grid a = nullptr, b = nullptr;
+    dexel_status s = dexel_create(&dq, &a);
+    if (s == DEXEL_OK) {
+      dq.stream = a->stream;   // the result handle shares the slab's stream
+      s = dexel_create(&dq, &b);
+    }
+    if (s != DEXEL_OK) {
+      const std::string msg = g_err;
+      dexel_destroy(a);
+      dexel_pipe_destroy(p);
+      g_err = msg;
+      return s;
+    }
+    p->src.push_back(a);
+    p->dst.push_back(b);
+  }
+  *out = p;
+  return DEXEL_OK;
+}
+
+void dexel_pipe_destroy(dexel_pipe p) {
+  if (!p) return;
+  for (dexel_grid g : p->dst) dexel_destroy(g);   // (before src: they borrow its stream)
+  for (dexel_grid g : p->src) dexel_destroy(g);
+  delete p;
+}
+
+dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const uint64_t* offsets,
+                            const float* endpoints, uint64_t* out_offsets, float* out_endpoints, uint64_t cap,
+                            uint64_t* n_out) {
+  g_err.clear();
+  if (!p || !offsets || !out_offsets || !n_out) return fail(DEXEL_EINVAL, "NULL argument");
+  if (op != OP_DILATE && op != OP_ERODE && op != OP_SHELL) return fail(DEXEL_EINVAL, "op must be 0, 1 or 2");
+  const int S = p->nslabs, nx = p->d.nx, ny = p->d.ny;
+  const int64_t ncol = (int64_t)nx * ny;
+  if (offsets[0] != 0 || (offsets[ncol] > 0 && !endpoints)) return fail(DEXEL_EINVAL, "bad input CSR");
+  int Ra, Rb;
+  dexel_status s;
+  if ((s = check_radius(r_a, p->d.spacing, &Ra))) return s;
+  if ((s = check_radius(op == OP_SHELL ? r_b : r_a, p->d.spacing, &Rb))) return s;
+  const int R = Ra > Rb ? Ra : Rb;
+  *n_out = 0;
+  PipeSync Q;
+  // rows [a, b) of the host CSR as a slice: offsets from a*nx, endpoints from its first interval
+  auto slice = [&](int a, int b, const uint64_t*& off, const float*& ep, uint64_t& n) {
+    off = offsets + (int64_t)a * nx;
+    n = offsets[(int64_t)b * nx] - off[0];
+    ep = endpoints ? endpoints + 2 * off[0] : nullptr;
+  };
+  std::thread up([&] {
+    for (int q = 0; q < S; ++q) {
+      {
+        std::lock_guard<std::mutex> lk(Q.mu);
+        if (Q.err) return;
+      }
+      dexel_grid g = p->src[q];
+      const int y0 = g->d.y0, y1 = g->d.y1;
+      const int lo = y0 < R ? y0 : R, hi = ny - y1 < R ? ny - y1 : R;
+      const uint64_t* off;
+      const float* ep;
+      uint64_t n;
+      slice(y0, y1, off, ep, n);
+      dexel_status e = upload_impl(g, off, ep, n, 0, true);
+      if (!e) {
+        slice(y0 - lo, y0, off, ep, n);
+        e = upload_halo_impl(g, 0, off, ep, lo, n, 0, true);
+      }
+      if (!e) {
+        slice(y1, y1 + hi, off, ep, n);
+        e = upload_halo_impl(g, 1, off, ep, hi, n, 0, true);
+      }
+      if (e) return Q.fail_with(e);
+      std::lock_guard<std::mutex> lk(Q.mu);
+      Q.uploaded = q + 1;
+      Q.cv.notify_all();
+    }
+  });
+  uint64_t total = 0;
+  std::thread down([&] {
+    for (int q = 0; q < S; ++q) {
+      {
+        std::unique_lock<std::mutex> lk(Q.mu);
+        Q.cv.wait(lk, [&] { return Q.computed > q || Q.err; });
+        if (Q.err) return;
+      }
+      dexel_grid g = p->dst[q];
+      if (total + g->n > cap) {
+        fail(DEXEL_EOVERFLOW, "capacity " + std::to_string(cap) + " < the result's intervals");
+        return Q.fail_with(DEXEL_EOVERFLOW);
+      }
+      uint64_t* o = out_offsets + (int64_t)g->d.y0 * nx;
+      const dexel_status e = dexel_download(g, o, out_endpoints ? out_endpoints + 2 * total : nullptr, cap - total, 0);
+      if (e) return Q.fail_with(e);
+      if (total)
+        for (int64_t c = 0; c <= g->ncol; ++c) o[c] += total;
+      total += g->n;
+    }
+  });
+  for (int q = 0; q < S; ++q) {
+    {
+      std::unique_lock<std::mutex> lk(Q.mu);
+      Q.cv.wait(lk, [&] { return Q.uploaded > q || Q.err; });
+      if (Q.err) break;
+    }
+    const dexel_status e = run_op(op, p->src[q], r_a, op == OP_SHELL ? r_b : r_a, p->dst[q]);
+    if (e) {
+      Q.fail_with(e);
+      break;
+    }
+    std::lock_guard<std::mutex> lk(Q.mu);
+    Q.computed = q + 1;
+    Q.cv.notify_all();
+  }
+  up.join();
+  down.join();
+  if (Q.err) {
+    g_err = Q.msg;
+    return Q.err;
+  }
+  *n_out = total;
   return DEXEL_OK;
 }
 

@@ -41,6 +41,12 @@ __global__ void validate_kernel(const uint64_t* __restrict__ off, const float* _
   if (!ok) atomicMin(first_bad, (unsigned long long)c);
 }
 
+// offsets of a CSR slice -> offsets from 0 (dexel_pipe_run uploads row slabs of one host CSR)
+__global__ void rebase_kernel(uint64_t* __restrict__ off, int64_t n, uint64_t base) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) off[c] -= base;
+}
+
 // ------------------------------------------------------------------ pass 1
 // The rows an op reads, in "extended" numbering 0 .. nrows-1: up to three CSR segments stacked
 // along y -- the halo rows below the slab (segment 0: received from rank g-1, DESIGN.md
