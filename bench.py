@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--r", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-slabs", type=int, default=8,
+    ap.add_argument("--e2e-slabs", type=int, default=-1,
                     help="y-slabs of the streamed host-to-host op (dexel_pipe_run) the e2e number is measured "
-                         "with at N=1; 0: only the serial upload + op + download")
+                         "with at N=1; -1: the library's suggestion (dexel_pipe_suggest_slabs; 1 = serial); "
+                         "0: only the serial upload + op + download")
     ap.add_argument("--cpu-rows", type=int, default=None, help="rows in the oracle band sample")
     a = ap.parse_args()
     a.op = a.op or DEFAULT_OP[a.config]
@@ -479,6 +480,10 @@ def run_b200(a, rank, world, local_rank):
         e2e = {"value": ncol / (e_ms / 1e3), "unit": "columns/s",
                "h2d_bytes_per_step": byts[0], "d2h_bytes_per_step": byts[1], "ms_per_step": e_ms,
                "api": "dexel_upload + op + dexel_download (serial)"}
+        if a.e2e_slabs < 0:
+            a.e2e_slabs = dx.Pipe.suggest_slabs(host.nx, host.ny, a.r, getattr(host, "spacing", 1.0))
+            if a.e2e_slabs == 1:
+                a.e2e_slabs = 0        # the library suggests no split: the serial calls are the e2e path
         if world == 1 and a.e2e_slabs > 0 and a.op in ("dilate", "erode", "shell"):
             # the streamed host-to-host call (dexel_pipe_run): the same pinned host CSRs, cut into
             # y-slabs so the upload of slab q+1, the op on slab q and the download of slab q-1 overlap;

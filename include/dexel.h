@@ -254,6 +254,9 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
                             const float* endpoints, uint64_t* out_offsets, float* out_endpoints,
                             uint64_t capacity, uint64_t* n_out);
 void dexel_pipe_destroy(dexel_pipe p);   /* NULL-safe */
+/* The slab count measured best for grid d and radius r on B200: slabs of at least
+ * max(512, 32 floor(r/s)) rows, at most 8 slabs; 1 = do not split (use the serial calls). */
+int dexel_pipe_suggest_slabs(const dexel_desc* d, float r);
 
 /* Route device allocations through a caller allocator (e.g. the PyTorch
  * caching allocator).  NULL,NULL restores cudaMallocAsync/cudaFreeAsync.

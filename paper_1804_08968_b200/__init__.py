@@ -28,7 +28,8 @@ EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel
            "dexel_download", "dexel_pass1", "dexel_sync", "dexel_destroy", "dexel_last_error",
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows", "dexel_nccl_unique_id", "dexel_nccl_comm_init", "dexel_nccl_comm_destroy",
-           "dexel_link_slabs", "dexel_pipe_create", "dexel_pipe_run", "dexel_pipe_destroy"]
+           "dexel_link_slabs", "dexel_pipe_create", "dexel_pipe_run", "dexel_pipe_destroy",
+           "dexel_pipe_suggest_slabs"]
 
 
 class DexelError(RuntimeError):
@@ -106,6 +107,7 @@ def lib():
             "dexel_pipe_run": ([vp, ctypes.c_int, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp, u64, u64p],
                                ctypes.c_int),
             "dexel_pipe_destroy": ([vp], None),
+            "dexel_pipe_suggest_slabs": ([ctypes.POINTER(dexel_desc), ctypes.c_float], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -283,6 +285,11 @@ class Pipe:
         h = ctypes.c_void_p()
         _check(lib().dexel_pipe_create(ctypes.byref(self.desc), nslabs, ctypes.byref(h)))
         self.h = h
+
+    @staticmethod
+    def suggest_slabs(nx: int, ny: int, r: float, spacing: float = 1.0) -> int:
+        d = dexel_desc(nx, ny, spacing, 0.0, 0.0, 1.0, 0, None, None, 0, 1, 0, ny)
+        return int(lib().dexel_pipe_suggest_slabs(ctypes.byref(d), r))
 
     def run(self, op: str, r_a: float, r_b: float, off, ep, out_off, out_ep) -> int:
         """host CSR (off, ep) -> host CSR written into (out_off, out_ep); returns the interval count.

@@ -2133,6 +2133,18 @@ dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out)
   return DEXEL_OK;
 }
 
+// Slab count for a grid and radius: slabs of at least max(512, 32 R) rows (the halo rows' pass 1 and
+// levels stay under ~6% of a slab's; smaller slabs also pay the per-op fixed costs more often), at
+// most 8 (measured on B200, profiles/r02_pipe_e2e.md: C5 r=16 best at 8, C4 r=16 at 4; C4 r=64 and
+// the 512^2 grid lose with any split -> 1).
+int dexel_pipe_suggest_slabs(const dexel_desc* d, float r) {
+  if (!d || d->ny < 1 || !(d->spacing > 0) || !(r >= 0)) return 1;
+  const double R = std::floor((double)r / d->spacing);
+  const double rows = std::max(512.0, 32.0 * R);
+  const int s = (int)((double)d->ny / rows);
+  return s < 1 ? 1 : (s > 8 ? 8 : s);
+}
+
 void dexel_pipe_destroy(dexel_pipe p) {
   if (!p) return;
   for (dexel_grid g : p->dst) dexel_destroy(g);   // (before src: they borrow its stream)

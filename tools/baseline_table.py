@@ -5,7 +5,7 @@ import sys
 
 rows = [json.loads(l) for l in open(sys.argv[1]) if l.strip().startswith("{")]
 par = json.load(open(sys.argv[2]))
-print("| config | op | r | GPUs | GPU columns/s (ms/op) | e2e columns/s | dominant kernel: algorithmic GB/s (fraction of 6523 measured) "
+print("| config | op | r | GPUs | GPU columns/s (ms/op) | e2e columns/s | dominant kernel: algorithmic GB/s (fraction of the measured 6456 GB/s) "
       "| oracle columns/s | host cores | parity (max error, count mismatches, columns compared) |")
 print("|---|---|---|---|---|---|---|---|---|---|")
 for d in rows:
