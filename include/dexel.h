@@ -255,7 +255,8 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
                             uint64_t capacity, uint64_t* n_out);
 void dexel_pipe_destroy(dexel_pipe p);   /* NULL-safe */
 /* The slab count measured best for grid d and radius r on B200: slabs of at least
- * max(512, 32 floor(r/s)) rows, at most 8 slabs; 1 = do not split (use the serial calls). */
+ * max(512, 32 R) rows, R = floor(r/s), at most 8 slabs, and 1 for R < 8 (the op is then
+ * shorter than its copies); 1 = do not split (use the serial calls). */
 int dexel_pipe_suggest_slabs(const dexel_desc* d, float r);
 
 /* Route device allocations through a caller allocator (e.g. the PyTorch

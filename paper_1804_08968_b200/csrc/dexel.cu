@@ -2135,11 +2135,14 @@ dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out)
 
 // Slab count for a grid and radius: slabs of at least max(512, 32 R) rows (the halo rows' pass 1 and
 // levels stay under ~6% of a slab's; smaller slabs also pay the per-op fixed costs more often), at
-// most 8 (measured on B200, profiles/r02_pipe_e2e.md: C5 r=16 best at 8, C4 r=16 at 4; C4 r=64 and
-// the 512^2 grid lose with any split -> 1).
+// most 8, and no split below R = 8: there the op is shorter than its copies, and uploads and
+// downloads running at once each slow down about 2x on this host, so overlapping them gains nothing
+// (measured on B200, profiles/r02_pipe_e2e.md: C5 r=16 best at 8 slabs, C4 r=16 and r=8 at 4; C4
+// r <= 4, C4 r=64 and the 512^2 grid lose with any split -> 1).
 int dexel_pipe_suggest_slabs(const dexel_desc* d, float r) {
   if (!d || d->ny < 1 || !(d->spacing > 0) || !(r >= 0)) return 1;
   const double R = std::floor((double)r / d->spacing);
+  if (R < 8) return 1;
   const double rows = std::max(512.0, 32.0 * R);
   const int s = (int)((double)d->ny / rows);
   return s < 1 ? 1 : (s > 8 ? 8 : s);
@@ -2168,6 +2171,13 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
   const int R = Ra > Rb ? Ra : Rb;
   *n_out = 0;
   PipeSync Q;
+  static const bool dbg = std::getenv("DEXEL_DEBUG") != nullptr;
+  const double t_run = now_s();
+  auto mark = [&](const char* what, int q, double t0) {   // DEXEL_DEBUG: the stages' timeline
+    if (dbg)
+      std::fprintf(stderr, "[dexel] pipe %s slab %d: %.3f .. %.3f ms\n", what, q, 1e3 * (t0 - t_run),
+                   1e3 * (now_s() - t_run));
+  };
   // rows [a, b) of the host CSR as a slice: offsets from a*nx, endpoints from its first interval
   auto slice = [&](int a, int b, const uint64_t*& off, const float*& ep, uint64_t& n) {
     off = offsets + (int64_t)a * nx;
@@ -2180,6 +2190,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
         std::lock_guard<std::mutex> lk(Q.mu);
         if (Q.err) return;
       }
+      const double t_up = now_s();
       dexel_grid g = p->src[q];
       const int y0 = g->d.y0, y1 = g->d.y1;
       const int lo = y0 < R ? y0 : R, hi = ny - y1 < R ? ny - y1 : R;
@@ -2197,6 +2208,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
         e = upload_halo_impl(g, 1, off, ep, hi, n, 0, true);
       }
       if (e) return Q.fail_with(e);
+      mark("upload", q, t_up);
       std::lock_guard<std::mutex> lk(Q.mu);
       Q.uploaded = q + 1;
       Q.cv.notify_all();
@@ -2210,6 +2222,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
         Q.cv.wait(lk, [&] { return Q.computed > q || Q.err; });
         if (Q.err) return;
       }
+      const double t_dn = now_s();
       dexel_grid g = p->dst[q];
       if (total + g->n > cap) {
         fail(DEXEL_EOVERFLOW, "capacity " + std::to_string(cap) + " < the result's intervals");
@@ -2221,6 +2234,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
       if (total)
         for (int64_t c = 0; c <= g->ncol; ++c) o[c] += total;
       total += g->n;
+      mark("download", q, t_dn);
     }
   });
   for (int q = 0; q < S; ++q) {
@@ -2229,17 +2243,20 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
       Q.cv.wait(lk, [&] { return Q.uploaded > q || Q.err; });
       if (Q.err) break;
     }
+    const double t_op = now_s();
     const dexel_status e = run_op(op, p->src[q], r_a, op == OP_SHELL ? r_b : r_a, p->dst[q]);
     if (e) {
       Q.fail_with(e);
       break;
     }
+    mark("op", q, t_op);
     std::lock_guard<std::mutex> lk(Q.mu);
     Q.computed = q + 1;
     Q.cv.notify_all();
   }
   up.join();
   down.join();
+  mark("run", S, t_run);
   if (Q.err) {
     g_err = Q.msg;
     return Q.err;
