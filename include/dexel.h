@@ -167,8 +167,10 @@ dexel_status dexel_shell_slices(dexel_grid src, float r_out, float r_in, dexel_g
  * Per column in fp64 without contraction: sphere chords [cz -+ sqrt(R^2 - dy^2 - dx^2)], the
  * unions of closed chords per sign, their difference, clipped to [zmin, zmax], shifted to the
  * local frame, rounded to fp32 and canonicalised -- bitwise the host generator
- * (dexelgen/dexelgen.c) that builds the configs.  A column needing more than 64 chord
- * intervals per sign or 32 output intervals -> DEXEL_EOVERFLOW (grid unchanged).
+ * (dexelgen/dexelgen.c) that builds the configs.  Columns with more than 64 disjoint chord
+ * intervals per sign or 32 output intervals make the library rasterise once more with large
+ * capacities (512 per sign; min(512, 2^30 / columns), at least 32, output intervals); a column
+ * beyond those -> DEXEL_EOVERFLOW (grid unchanged).
  * Synchronises the stream. */
 dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int nsph, const double* sph,
                                     const int32_t* sph_sign, int nbox, const double* box,

@@ -1338,7 +1338,8 @@ void preload_kernels(int device) {
   preload_one(pieces_to_csr);
   preload_one(raster_bin_count);
   preload_one(raster_bin_fill);
-  preload_one(raster_kernel);
+  preload_one(raster_kernel<RS_CAP>);
+  preload_one(raster_kernel<RS_CAP_BIG>);
   cudaGetLastError();
 }
 
@@ -1737,7 +1738,8 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   if ((s = T.get(sizeof(uint64_t) * (ntiles + 1), (void**)&dtoff))) return s;
   if ((s = T.get(sizeof(uint32_t) * (ntiles + 1) * 2, (void**)&tcnt))) return s;
   tcur = tcnt + ntiles + 1;
-  if ((s = T.get(sizeof(float2) * (size_t)RS_OUT * ncol + 16, (void**)&stage))) return s;
+  int out_cap = RS_OUT;
+  if ((s = T.get(sizeof(float2) * (size_t)out_cap * ncol + 16, (void**)&stage))) return s;
   if ((s = T.get(sizeof(uint32_t) * (ncol + 1), (void**)&cnt))) return s;
   if ((s = T.get(64, (void**)&flags))) return s;
   if (nsph) {
@@ -1760,17 +1762,37 @@ dexel_status dexel_rasterize_shapes(dexel_grid g, double zmin, double zmax, int 
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(flags, 0, 64, g->stream));
   RasterArgs A{nx, nrows, y0, zmin, zmax, zref, nsph, dsph, dss, nbox, dbox, dbs, dtoff, dtid, ntx,
-               stage, cnt, flags};
-  if (ntiles > 0) LAUNCH(T, K_RASTER, raster_kernel<<<(unsigned)ntiles, dim3(RT_X, RT_Y), 0, g->stream>>>(A));
+               stage, cnt, flags, out_cap};
+  if (ntiles > 0)
+    LAUNCH(T, K_RASTER, raster_kernel<RS_CAP><<<(unsigned)ntiles, dim3(RT_X, RT_Y), 0, g->stream>>>(A));
   CK(cudaGetLastError());
   unsigned hf = 0;
-  {
+  auto read_flag = [&]() -> cudaError_t {
     Readback rb{g};
     rb.add(0, flags, sizeof(hf));
-    CK(rb.wait());   // (the host shape vectors also stay alive until here)
+    const cudaError_t e = rb.wait();   // (the host shape vectors also stay alive until here)
     rb.get(0, &hf, sizeof(hf));
+    return e;
+  };
+  CK(read_flag());
+  if (hf) {
+    // a column outgrew the first attempt's capacities (64 chord intervals per sign, 32 output
+    // intervals): once more with 512-entry unions in local memory and a staging array of up to 512
+    // output intervals per column (at most ~8 GB: min(512, 2^30 / columns), at least 32)
+    const int64_t fit = ((int64_t)1 << 30) / (ncol > 0 ? ncol : 1);
+    out_cap = (int)std::max<int64_t>(RS_OUT, std::min<int64_t>(RS_CAP_BIG, fit));
+    if ((s = T.get(sizeof(float2) * (size_t)out_cap * ncol + 16, (void**)&stage))) return s;
+    CK(cudaMemsetAsync(flags, 0, 64, g->stream));
+    A.stage = stage;
+    A.out_cap = out_cap;
+    LAUNCH(T, K_RASTER, raster_kernel<RS_CAP_BIG><<<(unsigned)ntiles, dim3(RT_X, RT_Y), 0, g->stream>>>(A));
+    CK(cudaGetLastError());
+    CK(read_flag());
+    if (hf)
+      return fail(DEXEL_EOVERFLOW, "a column needs more than " + std::to_string(RS_CAP_BIG) +
+                                       " chord intervals per sign or " + std::to_string(out_cap) +
+                                       " output intervals");
   }
-  if (hf) return fail(DEXEL_EOVERFLOW, "a column needs more than 64 chord intervals per sign or 32 output intervals");
   // offsets, then the endpoints: the grid is replaced only now, into its own buffers when they
   // fit (a fresh allocation per call churns the stream-ordered pool); an error from here on
   // leaves the grid empty

@@ -28,8 +28,9 @@
 namespace dexel {
 
 constexpr int RT_X = 32, RT_Y = 8;
-constexpr int RS_CAP = 64;     // intervals per union (solid chords, void chords) of one column
-constexpr int RS_OUT = 32;     // output intervals per column (staging)
+constexpr int RS_CAP = 64;     // intervals per union (solid chords, void chords) of one column: first attempt
+constexpr int RS_OUT = 32;     // output intervals per column (staging): first attempt
+constexpr int RS_CAP_BIG = 512;   // second attempt after an overflow (16 KB of local memory per thread)
 
 struct RasterArgs {
   int nx, nrows, y0;           // local rows [0, nrows) are global rows y0 + jl
@@ -43,12 +44,14 @@ struct RasterArgs {
   const uint64_t* tile_off;    // [ntiles + 1]
   const int32_t* tile_ids;     // shape ids: sphere k -> k, box k -> nsph + k
   int ntx;                     // tiles per tile row
-  float2* stage;               // [RS_OUT][ncol]
+  float2* stage;               // [out_cap][ncol]
   uint32_t* cnt;               // [ncol]
   unsigned* flags;             // [0] a union or the output outgrew its capacity
+  int out_cap;                 // output intervals per column the staging array holds
 };
 
 // insert the closed interval [lo, hi] into the sorted disjoint union V[0..n) (touching merges)
+template <int CAP>
 __device__ __forceinline__ void rs_union_insert(double2* V, int& n, double lo, double hi, bool& ovf) {
   int p = 0;
   while (p < n && V[p].y < lo) ++p;
@@ -67,7 +70,7 @@ __device__ __forceinline__ void rs_union_insert(double2* V, int& n, double lo, d
     }
     return;
   }
-  if (n >= RS_CAP) {
+  if (n >= CAP) {
     ovf = true;
     return;
   }
@@ -76,13 +79,14 @@ __device__ __forceinline__ void rs_union_insert(double2* V, int& n, double lo, d
   ++n;
 }
 
+template <int CAP>
 __global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
   const int tile = blockIdx.x;
   const int tx = tile % A.ntx, ty = tile / A.ntx;
   const int i = tx * RT_X + threadIdx.x, jl = ty * RT_Y + threadIdx.y;
   const bool live = i < A.nx && jl < A.nrows;
   const double x = (double)i + 0.5, y = (double)(A.y0 + jl) + 0.5;
-  double2 P[RS_CAP], N[RS_CAP];
+  double2 P[CAP], N[CAP];
   int np = 0, nn = 0;
   bool ovf = false;
   for (uint64_t t = A.tile_off[tile]; t < A.tile_off[tile + 1]; ++t) {
@@ -118,8 +122,8 @@ __global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
     if (!live) continue;
     // (the host generator keeps chords with lo > hi out of nothing: none exist, h >= 0 and
     // boxes have z0 <= z1 by construction; a degenerate box still enters its union as given)
-    if (sg > 0) rs_union_insert(P, np, lo, hi, ovf);
-    else rs_union_insert(N, nn, lo, hi, ovf);
+    if (sg > 0) rs_union_insert<CAP>(P, np, lo, hi, ovf);
+    else rs_union_insert<CAP>(N, nn, lo, hi, ovf);
   }
   if (!live) return;
   const int64_t c = (int64_t)jl * A.nx + i;
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(RT_X* RT_Y) raster_kernel(RasterArgs A) {
       return;
     }
     if (!(a < b)) return;                   // zero length after rounding
-    if (k >= (uint32_t)RS_OUT) {
+    if (k >= (uint32_t)A.out_cap) {
       ovf = true;
       return;
     }

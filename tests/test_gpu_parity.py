@@ -637,6 +637,36 @@ def test_rasterize_shapes_random(dx, seed):
     g.close()
 
 
+def test_rasterize_shapes_many_chords(dx):
+    """Columns beyond the first attempt's capacities (64 chord intervals per sign, 32 output
+    intervals): 150 small spheres stacked along z, every third one carved by a void, plus 90 thin
+    box layers -- the library reruns with its large capacities; bitwise the host generator."""
+    nx, ny, zmin, zmax = 20, 12, 0.0, 640.0
+    k = np.arange(150)
+    sph = np.stack([np.full(150, 9.7), np.full(150, 6.2), 3.0 + 4.0 * k, np.full(150, 1.6)], axis=1)
+    voids = np.stack([np.full(50, 9.9), np.full(50, 6.1), 3.0 + 12.0 * np.arange(50), np.full(50, 0.6)], axis=1)
+    j = np.arange(90)
+    box = np.stack([np.full(90, 2.0), np.full(90, 6.0), np.full(90, 1.0), np.full(90, 5.0), 10.0 + 6.0 * j,
+                    11.5 + 6.0 * j], axis=1)
+    host = G.shapes(nx, ny, zmin, zmax, spheres=sph, voids=voids, boxes=box)
+    per_col = np.diff(host.off.astype(np.int64))
+    assert per_col.max() > 64                                   # (beyond both first-attempt capacities)
+    allsph = np.concatenate([sph, voids])
+    ss = np.concatenate([np.ones(150), -np.ones(50)]).astype(np.int32)
+    g = dx.Grid(nx, ny, host.z_lo, host.z_hi, host.z_ref)
+    dx.dexel_rasterize_shapes(g, zmin, zmax, allsph, ss, box, np.ones(90, np.int32))
+    off, ep = g.download()
+    assert np.array_equal(off.astype(np.uint64), host.off.astype(np.uint64))
+    assert np.array_equal(ep, host.ep)
+    # beyond the large capacities too: DEXEL_EOVERFLOW
+    k = np.arange(600)
+    sph = np.stack([np.full(600, 9.7), np.full(600, 6.2), 0.5 + 1.0 * k, np.full(600, 0.4)], axis=1)
+    with pytest.raises(dx.DexelError) as e:
+        dx.dexel_rasterize_shapes(g, zmin, zmax, sph, np.ones(600, np.int32))
+    assert e.value.status == dx.DEXEL_EOVERFLOW
+    g.close()
+
+
 def test_rasterize_shapes_errors(dx):
     host = G.config("C1")
     g = dx.Grid.from_host(host)
