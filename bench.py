@@ -492,12 +492,6 @@ def run_b200(a, rank, world, local_rank):
             pipe = dx.Pipe(host.nx, host.ny, host.z_lo, host.z_hi, ns, getattr(host, "z_ref", 0.0),
                            getattr(host, "spacing", 1.0), dev)
             r_b = a.r if a.op == "shell" else 0.0
-            hal = 0
-            for q in range(ns):
-                y0, y1 = host.ny * q // ns, host.ny * (q + 1) // ns
-                for lo, hi in ((max(0, y0 - R), y0), (y1, min(host.ny, y1 + R))):
-                    if hi > lo:
-                        hal += 8 * ((hi - lo) * host.nx + 1) + 8 * int(host.off[hi * host.nx] - host.off[lo * host.nx])
             for _ in range(max(a.warmup, 3)):     # (every slab handle settles its capacities in its first ops)
                 pipe.run(a.op, a.r, r_b, h_off, h_ep, o_off, o_ep)
             torch.cuda.synchronize()
@@ -505,13 +499,15 @@ def run_b200(a, rank, world, local_rank):
             for _ in range(ke):
                 nout_p = pipe.run(a.op, a.r, r_b, h_off, h_ep, o_off, o_ep)
             p_ms = 1e3 * (time.perf_counter() - t0) / ke     # (the call returns when the host CSR is complete)
+            p_h2d, p_d2h = pipe.last_bytes()       # counted by the library from the copies it made
+            slab_rows = [pipe.slab_rows(q) for q in range(ns)]
             pipe.close()
             assert nout_p == nout, (nout_p, nout)
             serial = e2e
             e2e = {"value": ncol / (p_ms / 1e3), "unit": "columns/s",
-                   "h2d_bytes_per_step": byts[0] + hal + 8 * (ns - 1), "d2h_bytes_per_step": byts[1] + 8 * (ns - 1),
+                   "h2d_bytes_per_step": p_h2d, "d2h_bytes_per_step": p_d2h,
                    "ms_per_step": p_ms, "api": f"dexel_pipe_run, {ns} y-slabs (upload / op / download overlapped)",
-                   "serial": serial}
+                   "slab_rows": slab_rows, "serial": serial}
 
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None

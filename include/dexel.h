@@ -242,7 +242,9 @@ const char* dexel_last_error(void);
  * of slab q-1 at the same time, on three host threads.  The result is bitwise the one
  * dexel_upload + op + dexel_download of the whole grid gives.
  *   d:         the whole grid on one device (nranks 1, y0 0, y1 ny, nccl_comm NULL; d->stream unused)
- *   nslabs:    1..ny (1: no overlap; the slabs' rows are ny*q/nslabs .. ny*(q+1)/nslabs)
+ *   nslabs:    1..ny (1: no overlap).  From 3 slabs on the first and the last slab get half the
+ *              rows of the others (the first upload and the last download are the copies no op
+ *              hides); dexel_pipe_slab_rows reports the partition
  *   op:        0 dilate (r_a), 1 erode (r_a), 2 shell (r_a = r_out, r_b = r_in)
  *   offsets, endpoints: HOST canonical CSR of the whole grid (nx*ny + 1 offsets from 0; pinned memory
  *              lets the copies overlap the kernels, pageable memory works but serialises them)
@@ -256,8 +258,13 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
                             const float* endpoints, uint64_t* out_offsets, float* out_endpoints,
                             uint64_t capacity, uint64_t* n_out);
 void dexel_pipe_destroy(dexel_pipe p);   /* NULL-safe */
+/* Rows [y0, y1) of slab q (0 <= q < nslabs). */
+dexel_status dexel_pipe_slab_rows(dexel_pipe p, int q, int32_t* y0, int32_t* y1);
+/* Bytes the last dexel_pipe_run copied host -> device (every slab's offsets and endpoints, its
+ * halo rows included) and device -> host (measurement). */
+dexel_status dexel_pipe_last_bytes(dexel_pipe p, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 /* The slab count measured best for grid d and radius r on B200: slabs of at least
- * max(512, 32 R) rows, R = floor(r/s), at most 8 slabs, and 1 for R < 8 (the op is then
+ * max(512, 32 R) rows, R = floor(r/s), at most 6 slabs, and 1 for R < 8 (the op is then
  * shorter than its copies); 1 = do not split (use the serial calls). */
 int dexel_pipe_suggest_slabs(const dexel_desc* d, float r);
 

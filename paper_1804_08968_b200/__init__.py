@@ -29,7 +29,7 @@ EXPORTS = ["dexel_create", "dexel_upload", "dexel_dilate", "dexel_erode", "dexel
            "dexel_set_allocator", "dexel_last_stats", "dexel_set_timing", "dexel_upload_halo",
            "dexel_download_rows", "dexel_nccl_unique_id", "dexel_nccl_comm_init", "dexel_nccl_comm_destroy",
            "dexel_link_slabs", "dexel_pipe_create", "dexel_pipe_run", "dexel_pipe_destroy",
-           "dexel_pipe_suggest_slabs"]
+           "dexel_pipe_suggest_slabs", "dexel_pipe_slab_rows", "dexel_pipe_last_bytes"]
 
 
 class DexelError(RuntimeError):
@@ -108,6 +108,9 @@ def lib():
                                ctypes.c_int),
             "dexel_pipe_destroy": ([vp], None),
             "dexel_pipe_suggest_slabs": ([ctypes.POINTER(dexel_desc), ctypes.c_float], ctypes.c_int),
+            "dexel_pipe_slab_rows": ([vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+                                     ctypes.c_int),
+            "dexel_pipe_last_bytes": ([vp, u64p, u64p], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -299,6 +302,17 @@ class Pipe:
         _check(lib().dexel_pipe_run(self.h, self.OPS[op], r_a, r_b, _ptr(off), _ptr(ep), _ptr(out_off),
                                     _ptr(out_ep), cap, ctypes.byref(n)))
         return n.value
+
+    def slab_rows(self, q: int):
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().dexel_pipe_slab_rows(self.h, q, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def last_bytes(self):
+        """(host -> device, device -> host) bytes the last run copied"""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().dexel_pipe_last_bytes(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:

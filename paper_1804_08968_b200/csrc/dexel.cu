@@ -2099,6 +2099,7 @@ struct dexel_pipe_s {
   dexel_desc d;
   int nslabs = 0;
   std::vector<dexel_grid> src, dst;
+  uint64_t h2d = 0, d2h = 0;   // bytes the last run copied (dexel_pipe_last_bytes)
 };
 
 namespace {
@@ -2133,8 +2134,16 @@ dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out)
     dq.stream = nullptr;   // a stream per slab (the stages overlap across slabs)
     dq.rank = q;
     dq.nranks = nslabs;
-    dq.y0 = (int)((int64_t)d->ny * q / nslabs);
-    dq.y1 = (int)((int64_t)d->ny * (q + 1) / nslabs);
+    // the first upload and the last download are the only copies no op hides: from 3 slabs on the
+    // first and the last slab get half the rows of the others (weights 1/2, 1, ..., 1, 1/2)
+    auto cut = [&](int t) -> int {   // first row of slab t
+      if (t <= 0) return 0;
+      if (t >= nslabs) return d->ny;
+      if (nslabs < 3 || d->ny < 2 * nslabs) return (int)((int64_t)d->ny * t / nslabs);
+      return (int)((int64_t)d->ny * (2 * t - 1) / (2 * (nslabs - 1)));
+    };
+    dq.y0 = cut(q);
+    dq.y1 = cut(q + 1);
     dexel_grid a = nullptr, b = nullptr;
     dexel_status s = dexel_create(&dq, &a);
     if (s == DEXEL_OK) {
@@ -2157,9 +2166,10 @@ dexel_status dexel_pipe_create(const dexel_desc* d, int nslabs, dexel_pipe* out)
 
 // Slab count for a grid and radius: slabs of at least max(512, 32 R) rows (the halo rows' pass 1 and
 // levels stay under ~6% of a slab's; smaller slabs also pay the per-op fixed costs more often), at
-// most 8, and no split below R = 8: there the op is shorter than its copies, and uploads and
+// most 6 (with the half-size end slabs C5 r=16 runs 147.5 ms with 6, 148.7 with 8, 151.1 with 10),
+// and no split below R = 8: there the op is shorter than its copies, and uploads and
 // downloads running at once each slow down about 2x on this host, so overlapping them gains nothing
-// (measured on B200, profiles/r02_pipe_e2e.md: C5 r=16 best at 8 slabs, C4 r=16 and r=8 at 4; C4
+// (measured on B200, profiles/r02_pipe_e2e.md: C4 r=16 and r=8 best at 4 slabs; C4
 // r <= 4, C4 r=64 and the 512^2 grid lose with any split -> 1).
 int dexel_pipe_suggest_slabs(const dexel_desc* d, float r) {
   if (!d || d->ny < 1 || !(d->spacing > 0) || !(r >= 0)) return 1;
@@ -2167,7 +2177,23 @@ int dexel_pipe_suggest_slabs(const dexel_desc* d, float r) {
   if (R < 8) return 1;
   const double rows = std::max(512.0, 32.0 * R);
   const int s = (int)((double)d->ny / rows);
-  return s < 1 ? 1 : (s > 8 ? 8 : s);
+  return s < 1 ? 1 : (s > 6 ? 6 : s);
+}
+
+dexel_status dexel_pipe_last_bytes(dexel_pipe p, uint64_t* h2d, uint64_t* d2h) {
+  g_err.clear();
+  if (!p || !h2d || !d2h) return fail(DEXEL_EINVAL, "NULL argument");
+  *h2d = p->h2d;
+  *d2h = p->d2h;
+  return DEXEL_OK;
+}
+
+dexel_status dexel_pipe_slab_rows(dexel_pipe p, int q, int32_t* y0, int32_t* y1) {
+  g_err.clear();
+  if (!p || !y0 || !y1 || q < 0 || q >= p->nslabs) return fail(DEXEL_EINVAL, "bad slab index");
+  *y0 = p->src[q]->d.y0;
+  *y1 = p->src[q]->d.y1;
+  return DEXEL_OK;
 }
 
 void dexel_pipe_destroy(dexel_pipe p) {
@@ -2206,6 +2232,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
     n = offsets[(int64_t)b * nx] - off[0];
     ep = endpoints ? endpoints + 2 * off[0] : nullptr;
   };
+  uint64_t h2d = 0;
   std::thread up([&] {
     for (int q = 0; q < S; ++q) {
       {
@@ -2220,13 +2247,16 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
       const float* ep;
       uint64_t n;
       slice(y0, y1, off, ep, n);
+      h2d += 8 * ((uint64_t)(y1 - y0) * nx + 1) + 8 * n;
       dexel_status e = upload_impl(g, off, ep, n, 0, true);
       if (!e) {
         slice(y0 - lo, y0, off, ep, n);
+        if (lo) h2d += 8 * ((uint64_t)lo * nx + 1) + 8 * n;
         e = upload_halo_impl(g, 0, off, ep, lo, n, 0, true);
       }
       if (!e) {
         slice(y1, y1 + hi, off, ep, n);
+        if (hi) h2d += 8 * ((uint64_t)hi * nx + 1) + 8 * n;
         e = upload_halo_impl(g, 1, off, ep, hi, n, 0, true);
       }
       if (e) return Q.fail_with(e);
@@ -2236,7 +2266,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
       Q.cv.notify_all();
     }
   });
-  uint64_t total = 0;
+  uint64_t total = 0, d2h = 0;
   std::thread down([&] {
     for (int q = 0; q < S; ++q) {
       {
@@ -2256,6 +2286,7 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
       if (total)
         for (int64_t c = 0; c <= g->ncol; ++c) o[c] += total;
       total += g->n;
+      d2h += 8 * ((uint64_t)g->ncol + 1) + 8 * g->n;
       mark("download", q, t_dn);
     }
   });
@@ -2279,6 +2310,8 @@ dexel_status dexel_pipe_run(dexel_pipe p, int op, float r_a, float r_b, const ui
   up.join();
   down.join();
   mark("run", S, t_run);
+  p->h2d = h2d;
+  p->d2h = d2h;
   if (Q.err) {
     g_err = Q.msg;
     return Q.err;

@@ -65,14 +65,14 @@ def test_python_api_raises_without_gpu(libpath):
 
 
 def test_pipe_suggest_slabs_rule(libpath):
-    """dexel_pipe_suggest_slabs is host logic: slabs of >= max(512, 32 R) rows, at most 8, at least 1."""
+    """dexel_pipe_suggest_slabs is host logic: slabs of >= max(512, 32 R) rows, at most 6, at least 1."""
     import paper_1804_08968_b200 as dx
     f = dx.Pipe.suggest_slabs
-    assert f(4096, 4096, 16.0) == 8 and f(2048, 2048, 16.0) == 4 and f(2048, 2048, 64.0) == 1
-    assert f(512, 512, 4.0) == 1 and f(64, 64, 3.0) == 1 and f(100000, 100000, 8.0) == 8
+    assert f(4096, 4096, 16.0) == 6 and f(2048, 2048, 16.0) == 4 and f(2048, 2048, 64.0) == 1
+    assert f(512, 512, 4.0) == 1 and f(64, 64, 3.0) == 1 and f(100000, 100000, 8.0) == 6
     assert f(2048, 2048, 4.0) == 1 and f(2048, 2048, 8.0) == 4      # R < 8: the copies dominate, no split
     assert f(2048, 2048, 16.0, spacing=0.5) == 2          # R = floor(r / s) = 32 -> 1024-row slabs
     for ny in (1, 511, 512, 1023, 1024, 5000):
         for r in (0.0, 0.5, 7.0, 33.0, 255.0):
             s = f(ny, ny, r)
-            assert 1 <= s <= 8 and (s == 1 or (r >= 8 and ny // s >= max(512, 32 * int(r))))
+            assert 1 <= s <= 6 and (s == 1 or (r >= 8 and ny // s >= max(512, 32 * int(r))))

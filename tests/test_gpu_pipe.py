@@ -101,6 +101,30 @@ def test_pipe_c2_pinned_repeated(dx):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_pipe_partition_and_bytes(dx):
+    host = G.random_grid(16, 40, 3, -4.0, 4.0, seed=9)
+    for ns in (1, 2, 3, 5, 8, 40):
+        pipe = dx.Pipe(16, 40, -4.0, 4.0, ns)
+        rows = [pipe.slab_rows(q) for q in range(ns)]
+        assert rows[0][0] == 0 and rows[-1][1] == 40
+        assert all(a < b for a, b in rows) and all(rows[q][1] == rows[q + 1][0] for q in range(ns - 1))
+        if 3 <= ns <= 8:                                    # the end slabs are about half the others
+            mid = rows[1][1] - rows[1][0]
+            assert rows[0][1] - rows[0][0] <= mid and rows[-1][1] - rows[-1][0] <= mid
+        off = np.ascontiguousarray(host.off, dtype=np.uint64)
+        ep = np.ascontiguousarray(host.ep, dtype=np.float32)
+        o_off, o_ep = np.zeros(16 * 40 + 1, np.uint64), np.zeros(2 * 20000, np.float32)
+        n = pipe.run("dilate", 2.0, 0.0, off, ep, o_off, o_ep)
+        h2d, d2h = pipe.last_bytes()
+        R, want = 2, 0
+        for a, b in rows:
+            for lo, hi in ((a, b), (max(0, a - R), a), (b, min(40, b + R))):
+                if hi > lo:
+                    want += 8 * ((hi - lo) * 16 + 1) + 8 * int(off[hi * 16] - off[lo * 16])
+        assert h2d == want and d2h == 8 * (16 * 40 + ns) + 8 * n
+        pipe.close()
+
+
 def test_pipe_empty_and_full(dx):
     nx, ny = 33, 9
     off = np.zeros(nx * ny + 1, np.uint64)
