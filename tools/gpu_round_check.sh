@@ -1,6 +1,6 @@
 # final check of the tree with the host pipeline (run under gpurun): all GPU tests, smoke, the default
 # bench line + reference arm, e2e lines of the workloads the library splits, the ncu launch list of the
-# default command.  usage: bash tools/gpu_pipe4.sh TAG
+# default command.  usage: bash tools/gpu_round_check.sh TAG
 tag=${1:-pipe4}
 DEXEL_PARITY_REPORT=gpurun_out/${tag}_parity.json timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
