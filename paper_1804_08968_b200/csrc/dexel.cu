@@ -78,6 +78,7 @@ struct dexel_grid_s {
   unsigned char* pin = nullptr;   // pinned host scratch for the small device->host readbacks
   // capacity hints carried between ops (grown on overflow)
   int lev_cap = 0, p2_acc = 0, p1_cap = 0;
+  int p2_peak = 0;     // longest pass-2 union any op on this handle held (sizes p2_acc)
   int lev_arena = 0;   // level-list arena entries per list once lev_cap is at LV_SLOT_MAX (0: 4 lev_cap)
   // the previous input CSR after a re-upload: the next upload of a similar size fills it
   // instead of allocating (an upload must not touch the current contents until validated)
@@ -1121,6 +1122,7 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
   const size_t opf_bytes = sizeof(unsigned) * OPF_WORDS + sizeof(unsigned long long) * scan_status_words((uint64_t)ncol);
   if ((s = T.get(opf_bytes, (void**)&opf))) return s;
   int acc = src->p2_acc > 0 ? src->p2_acc : 32;
+  static const bool no_acc_fit = std::getenv("DEXEL_P2_ACC") != nullptr || std::getenv("DEXEL_P2_NOFIT") != nullptr;
   float2* stage = nullptr;
   // Every capacity of the op (piece slots and arena, level slots and arena, the pass-2
   // accumulator, dst's buffer) is checked ONCE, at the end: kernels raise flags instead of the
@@ -1211,6 +1213,15 @@ dexel_status run_op_impl(int op, dexel_grid src, float r_a, float r_b, dexel_gri
       stats.p2_acc = acc;
       stats.lev_cap = lev_cap_used;
       dst->n = nout;
+      // size the next ops' accumulator by the longest union any op on this handle has held (rounded
+      // up to a multiple of 4): a shorter accumulator is less shared memory per warp, so more resident
+      // warps for the latency-bound pass 2 (measured, profiles/r02_p2_acc_times.txt: C5 needs 17-20
+      // entries; 32 -> 20 runs the op 133.0 -> 127.1 ms, C4 r=16 11.35 -> 10.88).  The handle's
+      // maximum, not the last op's: alternating ops do not rerun each other.
+      if (acc <= (int)(P2_SMEM_MAX / (32 * sizeof(float2))) - 2 * P2_R - 2 && !no_acc_fit) {
+        src->p2_peak = std::max(src->p2_peak, (int)hf[OPF_P2_PEAK]);
+        src->p2_acc = std::max(8, (src->p2_peak + 3) / 4 * 4);
+      }
       break;
     }
     // something overflowed: grow it (kept on the handle for later ops) and rerun the op.  Only the

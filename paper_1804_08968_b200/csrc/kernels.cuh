@@ -106,6 +106,7 @@ enum OpFlag {
   OPF_LV_LONGEST = 3,
   OPF_P2_ACC = 4,      // a pass-2 union longer than the accumulator: its length
   OPF_OUT_FIT = 5,     // the output did not fit dst's buffer (compaction skipped)
+  OPF_P2_PEAK = 6,     // the longest pass-2 union any column held during the op (sizes the next op's accumulator)
   OPF_WORDS = 16,      // (+ u64 statistics from word 8: n_mid, n_lev)
 };
 

@@ -39,6 +39,7 @@ struct Acc {
   float2* v;   // v[t * s]: shared memory (s = T, a compile-time constant) or global (the band's columns)
   int64_t s;
   int n;
+  int hw = 0;  // the most intervals it held (insertions only raise it: one max per insertion)
 };
 
 struct Cursor {
@@ -70,6 +71,7 @@ __device__ __forceinline__ void acc_add(Acc& A, Cursor& C, float a, float b, int
     }
     for (int t = A.n; t >= C.p; --t) A.v[(t + 1) * A.s] = A.v[t * A.s];
     ++A.n;
+    A.hw = max(A.hw, A.n);
     C.n1 = C.w.x;
     C.w = make_float2(a, b);
     A.v[C.p * A.s] = C.w;
@@ -259,6 +261,12 @@ __global__ void __launch_bounds__(T, 640 / T) pass2s_kernel(LevelSlots A, LevelS
   }
   ocnt[c] = n;
   if (need) atomicMax(flags + OPF_P2_ACC, need);
+  // the longest union of the op (one atomic per warp): the host sizes the next op's accumulator by it
+  // -- a shorter accumulator is less shared memory per warp, so more resident warps for this
+  // latency-bound kernel
+  const unsigned am = __activemask();
+  const unsigned pk = __reduce_max_sync(am, (unsigned)U.hw);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) atomicMax(flags + OPF_P2_PEAK, pk);
 }
 
 inline size_t pass2_smem_bytes(int op, int acc, int T, bool gacc = false) {
