@@ -264,6 +264,49 @@ def test_torch_allocator_hook(dx):
 
 
 
+def test_pass2_accumulator_fitted_to_the_handle(dx):
+    """The pass-2 accumulator follows the longest union any op on the handle held (a multiple of 4,
+    at least 8; default 32 for the first op): the fitted ops give bitwise the first op's result,
+    the capacity never falls when ops alternate, and an op that needs more than the fitted
+    capacity (a larger radius after a small one: more merged lists, then a many-layer input
+    uploaded into the same handle) reruns and still matches the oracle."""
+    host = G.random_grid(64, 40, 4, -16.0, 16.0, seed=31)
+    src = dx.Grid.from_host(host)
+    dst = dx.Grid.like(src)
+    dx.dexel_dilate(src, 2.0, dst)
+    first, cap0 = dst.download(), dst.stats()["capacities"]["p2_acc"]
+    dx.dexel_dilate(src, 2.0, dst)
+    again, cap1 = dst.download(), dst.stats()["capacities"]["p2_acc"]
+    assert cap0 == 32 and 8 <= cap1 <= 32 and cap1 % 4 == 0
+    assert np.array_equal(first[0], again[0]) and np.array_equal(first[1], again[1])
+    caps = []
+    for r in (0.5, 6.0, 0.5, 6.0, 0.5):                       # alternating ops on one handle
+        dx.dexel_shell(src, r, r, dst)
+        off, ep = dst.download()
+        check(off, ep, run_oracle(host, "shell", r), what=f"fitted accumulator shell r={r}")
+        caps.append(dst.stats()["capacities"]["p2_acc"])
+    assert caps[2:] == sorted(caps[2:]) and caps[4] == caps[3]  # settled at the handle's maximum
+    # a column-rich input into the same handle: unions far longer than the fitted capacity
+    rs = np.random.default_rng(5)
+    cols = []
+    for c in range(64 * 40):
+        k = 60 if c % 7 == 0 else 2
+        z = np.sort(rs.uniform(-15.5, 15.5, 2 * k)).astype(np.float32)
+        z = z[: 2 * (len(np.unique(z)) // 2)]
+        cols.append(np.unique(z).reshape(-1, 2) if len(np.unique(z)) == len(z) else np.zeros((0, 2), np.float32))
+    off = np.zeros(64 * 40 + 1, np.uint64)
+    np.cumsum([len(c) for c in cols], out=off[1:])
+    ep = np.concatenate([c.reshape(-1) for c in cols]).astype(np.float32)
+    rich = G.Grid(64, 40, off, ep, host.z_lo, host.z_hi)
+    src.upload(off, ep)
+    dx.dexel_dilate(src, 0.05, dst)
+    o2, e2 = dst.download()
+    check(o2, e2, run_oracle(rich, "dilate", 0.05), what="fitted accumulator, many-layer input")
+    assert dst.stats()["capacities"]["p2_acc"] > caps[-1]
+    src.close()
+    dst.close()
+
+
 @pytest.mark.parametrize("lev_cap,acc,band,p1cap", [("1", "1", "3", "1"), ("2", "4", "7", "6")])
 def test_capacity_regrowth(dx, lev_cap, acc, band, p1cap):
     """Start every capacity at its minimum (level slots per list, pass-2 accumulator:
