@@ -8,7 +8,7 @@ for a in "$@"; do
   timeout 300 python tools/run_op.py $1 $2 $3 1 > gpurun_out/${tag}_${name}_runop.log 2>&1 || continue
   PROFILE_LAST=1 timeout 900 ncu --set full --clock-control none --profile-from-start off \
     -k regex:"p1[gs]_kernel|levels_kernel|pass2s_kernel" -c 60 \
-    -o /tmp/${tag}_${name} python tools/run_op.py $1 $2 $3 3 > gpurun_out/${tag}_${name}_ncu.log 2>&1
+    -f -o /tmp/${tag}_${name} python tools/run_op.py $1 $2 $3 3 > gpurun_out/${tag}_${name}_ncu.log 2>&1
   ncu -i /tmp/${tag}_${name}.ncu-rep --page raw --csv > /tmp/${tag}_${name}_raw.csv
   python tools/ncu_summary.py /tmp/${tag}_${name}_raw.csv "${tag} $1 $2 r=$3, one op, ncu --set full" \
     > gpurun_out/${tag}_${name}_ncu_summary.txt 2>&1
